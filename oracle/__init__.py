@@ -1,0 +1,238 @@
+"""oracle -- TEST INFRASTRUCTURE ONLY.
+
+Plain, slow, single-threaded CPU implementation of the xNRMF hot path
+(arXiv 2509.06220), written from the paper (see ``nrmf_oracle.c`` for the
+line-by-line citations).  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  It shares no code with ``paper_2509_06220_b200`` (the product), and
+the product never imports it.
+
+Functions
+  v1_hypot(x, y, dtype)              Listing 2
+  R_H(x)                             Listing 1, literal
+  nrmf(x, lanes=None, J=None)        the tile-lane tree
+  tiles(x, tau0, count)              tile values (sampled parity at full size)
+  cols(A, r, c, ld)                  column norms + Frobenius norm (e:F)
+  shard_norms(x, G)                  per-rank subtree values of the sharded tree
+  combine(values)                    R_H over a power-of-two padded list
+  exact(x)                           exactly rounded RN(sqrt(sum x^2))
+  relerr(r, ref, dtype)              e:relerr
+  ub_relerr_H(depth, dtype)          Thm 3 + e:reH upper bound for a depth-d tree
+
+Tree constants (frozen, tree version 1): fp64 lanes=64, J=64; fp32 lanes=128,
+J=32; tile T = 4096.  These are restated here from DESIGN.md §3, not imported
+from the CUDA side.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from fractions import Fraction
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "nrmf_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+TREE = {np.dtype(np.float64): (64, 64), np.dtype(np.float32): (128, 32)}
+EPS = {np.dtype(np.float64): 2.0 ** -53, np.dtype(np.float32): 2.0 ** -24}
+
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fno-finite-math-only",
+          "-fPIC", "-shared"]
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        i64, vp, ip = ctypes.c_int64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)
+        d, f = ctypes.c_double, ctypes.c_float
+        L.oracle_v1_hypot_d.argtypes = [d, d]; L.oracle_v1_hypot_d.restype = d
+        L.oracle_v1_hypot_s.argtypes = [f, f]; L.oracle_v1_hypot_s.restype = f
+        L.oracle_R_H_d.argtypes = [i64, vp]; L.oracle_R_H_d.restype = d
+        L.oracle_R_H_s.argtypes = [i64, vp]; L.oracle_R_H_s.restype = f
+        L.oracle_nrmf_tree_d.argtypes = [vp, i64, i64, i64, i64, ip]; L.oracle_nrmf_tree_d.restype = d
+        L.oracle_nrmf_tree_s.argtypes = [vp, i64, i64, i64, i64, ip]; L.oracle_nrmf_tree_s.restype = f
+        L.oracle_tiles_d.argtypes = [vp, i64, i64, i64, i64, i64, vp]; L.oracle_tiles_d.restype = ctypes.c_int
+        L.oracle_tiles_s.argtypes = [vp, i64, i64, i64, i64, i64, vp]; L.oracle_tiles_s.restype = ctypes.c_int
+        L.oracle_nrmf_cols_d.argtypes = [i64, i64, i64, vp, i64, i64, vp, vp]
+        L.oracle_nrmf_cols_d.restype = ctypes.c_int
+        L.oracle_nrmf_cols_s.argtypes = [i64, i64, i64, vp, i64, i64, vp, vp]
+        L.oracle_nrmf_cols_s.restype = ctypes.c_int
+        L.exact_nrm_d.argtypes = [vp, i64]; L.exact_nrm_d.restype = d
+        L.exact_nrm_s.argtypes = [vp, i64]; L.exact_nrm_s.restype = f
+        _lib = L
+    return _lib
+
+
+def _arr(x, dtype=None):
+    x = np.ascontiguousarray(x, dtype=dtype)
+    if x.dtype not in (np.float64, np.float32):
+        raise TypeError(f"oracle: unsupported dtype {x.dtype}")
+    return x
+
+
+def _is64(x) -> bool:
+    return x.dtype == np.float64
+
+
+def v1_hypot(x, y, dtype=np.float64):
+    """Listing 2, one pair.  Returns a numpy scalar of ``dtype``."""
+    if np.dtype(dtype) == np.float64:
+        return np.float64(lib().oracle_v1_hypot_d(float(x), float(y)))
+    return np.float32(lib().oracle_v1_hypot_s(float(np.float32(x)), float(np.float32(y))))
+
+
+def R_H(x):
+    """Listing 1 (scalar recursive, ceil split) with v1_hypot; n >= 1."""
+    x = _arr(x)
+    assert x.size >= 1
+    f = lib().oracle_R_H_d if _is64(x) else lib().oracle_R_H_s
+    return x.dtype.type(f(x.size, x.ctypes.data))
+
+
+def nrmf(x, lanes: int | None = None, J: int | None = None, p2_min: int = 1):
+    """The tile-lane tree.  lanes/J default to the production tree of x's dtype.
+    lanes=1, J>=n (power of two) is Listing 1; lanes=8 is Z_D with an
+    R-with-v1_hypot final reduction."""
+    x = _arr(x)
+    dl, dj = TREE[x.dtype]
+    lanes = dl if lanes is None else lanes
+    J = dj if J is None else J
+    assert lanes & (lanes - 1) == 0 and J & (J - 1) == 0
+    ok = ctypes.c_int(1)
+    f = lib().oracle_nrmf_tree_d if _is64(x) else lib().oracle_nrmf_tree_s
+    r = f(x.ctypes.data, x.size, lanes, J, p2_min, ctypes.byref(ok))
+    if not ok.value:
+        raise MemoryError("oracle: allocation failed")
+    return x.dtype.type(r)
+
+
+def tiles(x, tau0: int = 0, count: int | None = None, lanes=None, J=None):
+    """Tile values tau0 .. tau0+count-1 of the tile-lane tree of x."""
+    x = _arr(x)
+    dl, dj = TREE[x.dtype]
+    lanes = dl if lanes is None else lanes
+    J = dj if J is None else J
+    T = lanes * J
+    nt = -(-x.size // T)
+    count = nt - tau0 if count is None else count
+    out = np.empty(count, dtype=x.dtype)
+    f = lib().oracle_tiles_d if _is64(x) else lib().oracle_tiles_s
+    if not f(x.ctypes.data, x.size, lanes, J, tau0, count, out.ctypes.data):
+        raise MemoryError("oracle: allocation failed")
+    return out
+
+
+def cols(A, r: int, c: int, ld: int, lanes=None, J=None):
+    """Column norms of the column-major r x c matrix stored in flat A (leading
+    dimension ld), and the Frobenius norm (R_H over the padded column norms)."""
+    A = _arr(A)
+    dl, dj = TREE[A.dtype]
+    lanes = dl if lanes is None else lanes
+    J = dj if J is None else J
+    col = np.empty(c, dtype=A.dtype)
+    frob = np.zeros(1, dtype=A.dtype)
+    f = lib().oracle_nrmf_cols_d if _is64(A) else lib().oracle_nrmf_cols_s
+    if not f(r, c, ld, A.ctypes.data, lanes, J, col.ctypes.data, frob.ctypes.data):
+        raise MemoryError("oracle: allocation failed")
+    return col, A.dtype.type(frob[0])
+
+
+def combine(values):
+    """R_H over the list padded with +0 to a power of two (the rank tree)."""
+    v = _arr(values)
+    if v.size == 0:
+        return v.dtype.type(0)
+    p = 1
+    while p < v.size:
+        p <<= 1
+    pad = np.zeros(p, dtype=v.dtype)
+    pad[: v.size] = v
+    return R_H(pad)
+
+
+def shard_ranges(n: int, G: int, T: int = 4096):
+    """Canonical contiguous shards: NT = ceil(n/T) tiles,
+    P2 = pow2 >= NT; if G <= P2 rank g owns tiles [g*P2/G, (g+1)*P2/G), else
+    rank g < P2 owns tile g.  Returns [(offset, count, p2_local)] per rank
+    (p2_local = 0 for a rank that owns no part of the tree)."""
+    nt = -(-n // T)
+    P2 = 1
+    while P2 < nt:
+        P2 <<= 1
+    out = []
+    for g in range(G):
+        if G <= P2:
+            per = P2 // G
+            t0, t1 = g * per, (g + 1) * per
+            p2l = per
+        else:
+            t0, t1 = (g, g + 1) if g < P2 else (P2, P2)
+            p2l = 1 if g < P2 else 0
+        a, b = min(t0 * T, n), min(t1 * T, n)
+        out.append((a, b - a, p2l))
+    return out
+
+
+def shard_norms(x, G: int):
+    """Value of each rank's aligned subtree (oracle), in rank order."""
+    x = _arr(x)
+    dl, dj = TREE[x.dtype]
+    res = []
+    for (a, cnt, p2l) in shard_ranges(x.size, G, dl * dj):
+        if p2l == 0:
+            res.append(None)
+        else:
+            res.append(nrmf(x[a:a + cnt], p2_min=p2l))
+    return res
+
+
+def combine_ranks(values):
+    """Rank tree: R_H over the values of ranks that own part of the tree."""
+    vals = [v for v in values if v is not None]
+    return combine(np.array(vals, dtype=type(vals[0])))
+
+
+def exact(x):
+    """RN(sqrt(sum x_i^2)) computed exactly (integer superaccumulator)."""
+    x = _arr(x)
+    f = lib().exact_nrm_d if _is64(x) else lib().exact_nrm_s
+    return x.dtype.type(f(x.ctypes.data, x.size))
+
+
+def relerr(r, ref, dtype=np.float64) -> float:
+    """e:relerr: |ref - r| / (ref * eps_x), evaluated exactly."""
+    eps = Fraction(EPS[np.dtype(dtype)])
+    R, F = Fraction(float(r)), Fraction(float(ref))
+    if F == 0:
+        return 0.0 if R == 0 else float("inf")
+    return float(abs(F - R) / (F * eps))
+
+
+def reH_plus(dtype=np.float64):
+    """1 + eps'^+ of e:reH as an mpmath number (256 bits)."""
+    import mpmath
+    mpmath.mp.prec = 256
+    e = mpmath.mpf(EPS[np.dtype(dtype)])
+    return (1 + e) ** mpmath.mpf(2.5) * mpmath.sqrt(1 + e * (2 + e) / 2)
+
+
+def ub_relerr_H(depth: int, dtype=np.float64) -> float:
+    """Upper bound on relerr (in eps units) for a v1_hypot tree whose longest
+    root-to-leaf path has `depth` rounding nodes: Thm 3 (e:8) with equal
+    children bounds gives 1+eps_[n]^+ = (1+eps_[k]^+)(1+eps'^+) per level."""
+    import mpmath
+    mpmath.mp.prec = 256
+    e = mpmath.mpf(EPS[np.dtype(dtype)])
+    return float(((reH_plus(dtype)) ** depth - 1) / e)
