@@ -59,6 +59,8 @@ def lib():
         d, f = ctypes.c_double, ctypes.c_float
         L.oracle_v1_hypot_d.argtypes = [d, d]; L.oracle_v1_hypot_d.restype = d
         L.oracle_v1_hypot_s.argtypes = [f, f]; L.oracle_v1_hypot_s.restype = f
+        L.oracle_v1_hypot_array_d.argtypes = [i64, vp, vp, vp]; L.oracle_v1_hypot_array_d.restype = None
+        L.oracle_v1_hypot_array_s.argtypes = [i64, vp, vp, vp]; L.oracle_v1_hypot_array_s.restype = None
         L.oracle_R_H_d.argtypes = [i64, vp]; L.oracle_R_H_d.restype = d
         L.oracle_R_H_s.argtypes = [i64, vp]; L.oracle_R_H_s.restype = f
         L.oracle_nrmf_tree_d.argtypes = [vp, i64, i64, i64, i64, ip]; L.oracle_nrmf_tree_d.restype = d
@@ -91,6 +93,17 @@ def v1_hypot(x, y, dtype=np.float64):
     if np.dtype(dtype) == np.float64:
         return np.float64(lib().oracle_v1_hypot_d(float(x), float(y)))
     return np.float32(lib().oracle_v1_hypot_s(float(np.float32(x)), float(np.float32(y))))
+
+
+def v1_hypot_array(x, y):
+    """Listing 2 applied elementwise to two equal-length arrays."""
+    x = _arr(x)
+    y = _arr(y, x.dtype)
+    assert x.size == y.size
+    out = np.empty_like(x)
+    f = lib().oracle_v1_hypot_array_d if _is64(x) else lib().oracle_v1_hypot_array_s
+    f(x.size, x.ctypes.data, y.ctypes.data, out.ctypes.data)
+    return out
 
 
 def R_H(x):

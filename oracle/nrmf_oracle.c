@@ -56,6 +56,12 @@ double oracle_v1_hypot_d(double x, double y)
     return (M * s);                    /* M*sqrt(1+(m/M)^2) */
 }
 
+/* Listing 2 applied to n pairs (a convenience loop for large pin sets). */
+void oracle_v1_hypot_array_d(int64_t n, const double *x, const double *y, double *out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_v1_hypot_d(x[i], y[i]);
+}
+
 /* R_S substitutions double->float, fabs->fabsf, hypot->hypotf. */
 float oracle_v1_hypot_s(float x, float y)
 {
@@ -68,6 +74,11 @@ float oracle_v1_hypot_s(float x, float y)
     const float S = fmaf(Q, Q, 1.0f);
     const float s = sqrtf(S);
     return (M * s);
+}
+
+void oracle_v1_hypot_array_s(int64_t n, const float *x, const float *y, float *out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_v1_hypot_s(x[i], y[i]);
 }
 
 /* ------------------------------------------------------------------------- */

@@ -1,0 +1,285 @@
+"""paper_2509_06220_b200 -- B200-native xNRMF (arXiv 2509.06220).
+
+Thin Python binding over the C ABI in ``include/nrmf.h`` (``libnrmf.so``,
+hand-written sm_100a CUDA).  This module only marshals arguments: every step
+of the norm runs in the library's kernels.  PyTorch provides device memory,
+streams and process groups.  There is no CPU fallback: if ``libnrmf.so`` is
+missing or a call fails, an exception is raised.
+
+    norm(x)                 ||x||_F of a contiguous fp32/fp64 tensor (CUDA, or
+                            host memory streamed through the GPU)
+    norm_complex(z)         ||z||_F of a complex64/complex128 tensor
+    cols(A)                 (column norms, Frobenius norm) of a column-major matrix
+    dist(x_local, n_global) ||x||_F of an array sharded over torch.distributed ranks
+    shard(n_global, world, rank) -> (offset, count) canonical shard
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from . import _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnrmf.so")
+
+NRMF_OK = 0
+_lib = None
+_lock = threading.Lock()
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libnrmf.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
+        L.nrmf_status_str.argtypes = [i32]; L.nrmf_status_str.restype = ctypes.c_char_p
+        L.nrmf_tree_version.argtypes = []; L.nrmf_tree_version.restype = i32
+        L.nrmf_tree_params.argtypes = [i32, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+        L.nrmf_workspace_bytes.argtypes = [i64, i32]; L.nrmf_workspace_bytes.restype = sz
+        L.nrmf_cols_workspace_bytes.argtypes = [i64, i64, i32]; L.nrmf_cols_workspace_bytes.restype = sz
+        L.nrmf_host_workspace_bytes.argtypes = [i64, i32]; L.nrmf_host_workspace_bytes.restype = sz
+        L.nrmf_dist_workspace_bytes.argtypes = [i64, i32, i32]; L.nrmf_dist_workspace_bytes.restype = sz
+        for f in ("nrmf_d", "nrmf_s", "nrmf_z_d", "nrmf_z_s", "nrmf_host_d", "nrmf_host_s"):
+            getattr(L, f).argtypes = [i64, vp, vp, vp, sz, vp]
+            getattr(L, f).restype = i32
+        for f in ("nrmf_cols_d", "nrmf_cols_s"):
+            getattr(L, f).argtypes = [i64, i64, i64, vp, vp, vp, vp, sz, vp]
+            getattr(L, f).restype = i32
+        for f in ("nrmf_dist_d", "nrmf_dist_s"):
+            getattr(L, f).argtypes = [i64, i64, i64, vp, vp, vp, sz, vp, vp]
+            getattr(L, f).restype = i32
+        L.nrmf_dist_shard.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.nrmf_dist_shard.restype = i32
+        L.nrmf_nccl_unique_id.argtypes = [ctypes.c_char_p]; L.nrmf_nccl_unique_id.restype = i32
+        L.nrmf_nccl_comm_init.argtypes = [i32, i32, ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.nrmf_nccl_comm_init.restype = i32
+        L.nrmf_nccl_comm_destroy.argtypes = [vp]; L.nrmf_nccl_comm_destroy.restype = i32
+        L.nrmf_debug_set_grid.argtypes = [i32]; L.nrmf_debug_set_grid.restype = i32
+        _lib = L
+    return _lib
+
+
+def lib():
+    """The loaded ctypes library (raises if it is not built)."""
+    return _load()
+
+
+def _check(status: int, what: str):
+    if status != NRMF_OK:
+        raise RuntimeError(f"{what}: {_load().nrmf_status_str(status).decode()}")
+
+
+def tree_version() -> int:
+    return _load().nrmf_tree_version()
+
+
+def tree_params(dtype) -> tuple[int, int, int]:
+    esz = torch.empty(0, dtype=dtype).element_size()
+    a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _check(_load().nrmf_tree_params(esz, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "tree_params")
+    return a.value, b.value, c.value
+
+
+# --------------------------------------------------------------- workspaces
+# Zero-filled once, cached per (device, stream, kind); the library leaves a
+# workspace ready for its next call.
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, device: torch.device, stream: torch.cuda.Stream, kind: str) -> torch.Tensor:
+    key = (device.index, stream.cuda_stream, kind)
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+def clear_workspaces():
+    _ws_cache.clear()
+
+
+def _elem(dtype) -> tuple[int, str]:
+    if dtype == torch.float64:
+        return 8, "d"
+    if dtype == torch.float32:
+        return 4, "s"
+    raise ValueError(f"nrmf: unsupported dtype {dtype} (float32/float64 only)")
+
+
+# --------------------------------------------------------------- public API
+def norm(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """||x||_F by the xNRMF tree (bitwise reproducible).
+
+    CUDA tensor: enqueued on the current stream, returns a 0-d CUDA tensor.
+    CPU tensor (pin it for copy/compute overlap): streamed through the current
+    CUDA device; synchronizes and returns a 0-d CPU tensor."""
+    if not x.is_contiguous():
+        raise ValueError("nrmf.norm: tensor must be contiguous")
+    esz, c = _elem(x.dtype)
+    L = _load()
+    n = x.numel()
+    if x.is_cuda:
+        dev = x.device
+        with torch.cuda.device(dev):
+            s = torch.cuda.current_stream(dev)
+            if out is None:
+                out = torch.empty((), dtype=x.dtype, device=dev)
+            ws = _workspace(L.nrmf_workspace_bytes(n, esz), dev, s, "vec")
+            f = L.nrmf_d if c == "d" else L.nrmf_s
+            _check(f(n, x.data_ptr() if n else None, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                     s.cuda_stream), "nrmf.norm")
+        return out
+    # host input
+    dev = torch.device("cuda", torch.cuda.current_device())
+    s = torch.cuda.current_stream(dev)
+    if out is None:
+        out = torch.empty((), dtype=x.dtype).pin_memory()
+    ws = _workspace(L.nrmf_host_workspace_bytes(n, esz), dev, s, "host")
+    f = L.nrmf_host_d if c == "d" else L.nrmf_host_s
+    _check(f(n, x.data_ptr() if n else None, out.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream),
+           "nrmf.norm(host)")
+    s.synchronize()
+    return out
+
+
+def norm_complex(z: torch.Tensor) -> torch.Tensor:
+    """||z||_F of a complex tensor = the real norm of its 2*numel interleaved
+    parts (e:F); bitwise equal to norm(torch.view_as_real(z))."""
+    if not z.is_complex():
+        raise ValueError("nrmf.norm_complex: complex tensor expected")
+    if not z.is_contiguous():
+        raise ValueError("nrmf.norm_complex: tensor must be contiguous")
+    zr = torch.view_as_real(z)
+    if not z.is_cuda:
+        return norm(zr.reshape(-1))
+    esz, c = _elem(zr.dtype)
+    L = _load()
+    dev = z.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream(dev)
+        out = torch.empty((), dtype=zr.dtype, device=dev)
+        ws = _workspace(L.nrmf_workspace_bytes(2 * z.numel(), esz), dev, s, "vec")
+        f = L.nrmf_z_d if c == "d" else L.nrmf_z_s
+        _check(f(z.numel(), zr.data_ptr() if z.numel() else None, out.data_ptr(), ws.data_ptr(),
+                 ws.numel(), s.cuda_stream), "nrmf.norm_complex")
+    return out
+
+
+def cols(A: torch.Tensor, frob: bool = True):
+    """Column norms and Frobenius norm of a column-major CUDA matrix
+    (A.stride(0) == 1, ld = A.stride(1)); e.g. ``B.t()`` of a row-major B."""
+    if A.dim() != 2:
+        raise ValueError("nrmf.cols: 2-D tensor expected")
+    r, c = A.shape
+    if not A.is_cuda:
+        raise ValueError("nrmf.cols: CUDA tensor expected")
+    if r > 1 and A.stride(0) != 1:
+        raise ValueError("nrmf.cols: column-major storage expected (stride(0) == 1)")
+    ld = A.stride(1) if c > 1 else max(r, 1)
+    if c > 1 and ld < r:
+        raise ValueError("nrmf.cols: leading dimension smaller than rows")
+    esz, ch = _elem(A.dtype)
+    L = _load()
+    dev = A.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream(dev)
+        col = torch.empty(c, dtype=A.dtype, device=dev)
+        fr = torch.empty((), dtype=A.dtype, device=dev) if frob else None
+        ws = _workspace(L.nrmf_cols_workspace_bytes(r, c, esz), dev, s, "cols")
+        f = L.nrmf_cols_d if ch == "d" else L.nrmf_cols_s
+        _check(f(r, c, ld, A.data_ptr() if A.numel() else None, col.data_ptr() if c else None,
+                 fr.data_ptr() if fr is not None else None, ws.data_ptr(), ws.numel(), s.cuda_stream),
+               "nrmf.cols")
+    return (col, fr) if frob else col
+
+
+def shard(n_global: int, world: int, rank: int) -> tuple[int, int]:
+    """Canonical contiguous shard (offset, count) of `rank` (nrmf_dist_shard)."""
+    off, cnt = ctypes.c_int64(), ctypes.c_int64()
+    _check(_load().nrmf_dist_shard(n_global, world, rank, ctypes.byref(off), ctypes.byref(cnt)),
+           "nrmf.shard")
+    return off.value, cnt.value
+
+
+class Comm:
+    """An NCCL communicator owned by the library, bootstrapped through a
+    torch.distributed process group (the 128-byte unique id is broadcast with
+    the group's own backend)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        L = _load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        idbuf = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(L.nrmf_nccl_unique_id(idbuf), "nccl unique id")
+        obj = [bytes(idbuf.raw)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        h = ctypes.c_void_p()
+        _check(L.nrmf_nccl_comm_init(self.world, self.rank, ctypes.c_char_p(obj[0]), ctypes.byref(h)),
+               "nccl comm init")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _load().nrmf_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
+_comms: dict = {}
+
+
+def comm_for(group=None) -> Comm:
+    key = (id(group), torch.cuda.current_device())
+    c = _comms.get(key)
+    if c is None:
+        c = Comm(group)
+        _comms[key] = c
+    return c
+
+
+def dist(x_local: torch.Tensor, n_global: int, group=None, comm: Comm | None = None,
+         out: torch.Tensor | None = None) -> torch.Tensor:
+    """||x||_F of an array of n_global elements sharded canonically over the
+    ranks of `group` (x_local = this rank's shard, see shard()).  Collective;
+    returns the same 0-d CUDA tensor bits on every rank."""
+    if not x_local.is_cuda or not x_local.is_contiguous():
+        raise ValueError("nrmf.dist: contiguous CUDA tensor expected")
+    esz, c = _elem(x_local.dtype)
+    comm = comm or comm_for(group)
+    off, cnt = shard(n_global, comm.world, comm.rank)
+    if x_local.numel() != cnt:
+        raise ValueError(f"nrmf.dist: rank {comm.rank} expects {cnt} elements, got {x_local.numel()}")
+    L = _load()
+    dev = x_local.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream(dev)
+        if out is None:
+            out = torch.empty((), dtype=x_local.dtype, device=dev)
+        ws = _workspace(L.nrmf_dist_workspace_bytes(n_global, comm.world, esz), dev, s, "dist")
+        f = L.nrmf_dist_d if c == "d" else L.nrmf_dist_s
+        _check(f(n_global, off, cnt, x_local.data_ptr() if cnt else None, out.data_ptr(), ws.data_ptr(),
+                 ws.numel(), comm.handle, s.cuda_stream), "nrmf.dist")
+    return out
+
+
+def _debug_set_grid(grid: int):
+    """Test hook: force the persistent grid size (0 = automatic)."""
+    _load().nrmf_debug_set_grid(grid)
+
+
+def build(force: bool = False) -> str:
+    return _build.build(force=force)

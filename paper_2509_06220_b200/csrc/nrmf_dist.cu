@@ -1,0 +1,205 @@
+// nrmf_dist.cu -- the rank level of the tree (a6 of DESIGN.md §8).
+//
+// e:hr: the norms of two disjoint parts combine by one hypot; the
+// paper's §5 suggests contiguous chunks per worker with hypot as
+// the reduction but warns that an unspecified reduction order breaks
+// reproducibility.  Here the order is fixed: every rank owns an aligned
+// subtree of the one global tile tree, reduces it locally (the same kernel as
+// nrmf_d), exchanges ONE scalar with ncclAllGather (NCCL has no user-defined
+// reduction and summing squares would reintroduce the overflow the method
+// avoids), and evaluates the top lg(world) levels itself.  Every rank gets the
+// same bits, equal to the 1-GPU result.
+//
+// NCCL is loaded with dlopen("libnccl.so.2") so that the process uses the
+// NCCL it already has (torch's) and libnrmf.so has no link-time dependency.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/nrmf.h"
+#include "nrmf_internal.h"
+
+namespace nrmf {
+namespace {
+
+constexpr int64_t kTileE = 4096;
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) =
+      nullptr;
+  bool ok = false;
+};
+
+NcclApi g_nccl;
+std::once_flag g_nccl_once;
+
+const NcclApi* nccl() {
+  std::call_once(g_nccl_once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) return;
+    g_nccl.GetUniqueId = reinterpret_cast<decltype(g_nccl.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    g_nccl.CommInitRank = reinterpret_cast<decltype(g_nccl.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    g_nccl.CommCount = reinterpret_cast<decltype(g_nccl.CommCount)>(dlsym(h, "ncclCommCount"));
+    g_nccl.CommUserRank = reinterpret_cast<decltype(g_nccl.CommUserRank)>(dlsym(h, "ncclCommUserRank"));
+    g_nccl.AllGather = reinterpret_cast<decltype(g_nccl.AllGather)>(dlsym(h, "ncclAllGather"));
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.CommCount &&
+                g_nccl.CommUserRank && g_nccl.AllGather;
+  });
+  return g_nccl.ok ? &g_nccl : nullptr;
+}
+
+int64_t pow2_ceil(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Canonical shard (nrmf.h): returns local subtree size p2_local (0 = none).
+int64_t shard(int64_t n, int world, int rank, int64_t* off, int64_t* cnt) {
+  const int64_t nt = (n + kTileE - 1) / kTileE;
+  const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
+  int64_t t0, t1, p2l;
+  if (world <= P2) {
+    const int64_t per = P2 / world;
+    t0 = rank * per;
+    t1 = t0 + per;
+    p2l = per;
+  } else if (rank < P2) {
+    t0 = rank;
+    t1 = rank + 1;
+    p2l = 1;
+  } else {
+    t0 = t1 = P2;
+    p2l = 0;
+  }
+  const int64_t a = std::min(t0 * kTileE, n), b = std::min(t1 * kTileE, n);
+  *off = a;
+  *cnt = b - a;
+  return p2l;
+}
+
+// workspace: [local tree ws][local value (256)][gathered (world entries)]
+size_t dist_ws(int64_t n, int world, size_t esz) {
+  const int64_t nt = (n + kTileE - 1) / kTileE;
+  const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
+  const int64_t p2l = world <= P2 ? P2 / world : 1;
+  return tree_workspace(p2l, esz) + 256 + align_up((size_t)world * esz, 256);
+}
+
+template <typename F>
+int dist_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, void* ws,
+              size_t ws_bytes, void* comm_v, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const NcclApi* api = nccl();
+  if (api == nullptr) return NRMF_ENCCL;
+  if (comm_v == nullptr || out == nullptr || ws == nullptr || n < 0) return NRMF_EINVAL;
+  if (count > 0 && x == nullptr) return NRMF_EINVAL;
+  if (reinterpret_cast<uintptr_t>(x) % sizeof(F) || reinterpret_cast<uintptr_t>(out) % sizeof(F))
+    return NRMF_EALIGN;
+  ncclComm_t comm = static_cast<ncclComm_t>(comm_v);
+  int world = 0, rank = 0;
+  if (api->CommCount(comm, &world) != ncclSuccess || api->CommUserRank(comm, &rank) != ncclSuccess)
+    return NRMF_ENCCL;
+  if (!is_pow2(world)) return NRMF_ESHARD;
+  int64_t off = 0, cnt = 0;
+  const int64_t p2l = shard(n, world, rank, &off, &cnt);
+  if (off != offset || cnt != count) return NRMF_ESHARD;
+  if (ws_bytes < dist_ws(n, world, sizeof(F))) return NRMF_EWORKSPACE;
+
+  const int64_t nt = (n + kTileE - 1) / kTileE;
+  const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
+  const int64_t p2ws = world <= P2 ? P2 / world : 1;
+  char* p = static_cast<char*>(ws);
+  const size_t tws = tree_workspace(p2ws, sizeof(F));
+  void* tree_ws = p;
+  F* local = reinterpret_cast<F*>(p + tws);
+  F* gathered = reinterpret_cast<F*>(p + tws + 256);
+
+  int st = NRMF_OK;
+  if (p2l > 0 && cnt > 0) {
+    st = tree_eval<F>(cnt, x, p2l, local, tree_ws, tws, s);
+  } else if (cudaMemsetAsync(local, 0, sizeof(F), s) != cudaSuccess) {
+    st = NRMF_ECUDA;  // rank owns an all-padding subtree (value +0) or none
+  }
+  if (st != NRMF_OK) return st;
+  const ncclDataType_t dt = sizeof(F) == 8 ? ncclFloat64 : ncclFloat32;
+  if (api->AllGather(local, gathered, 1, dt, comm, s) != ncclSuccess) return NRMF_ENCCL;
+  // rank tree: the top levels over the ranks that own part of the tree
+  const int64_t nr = std::min<int64_t>(world, P2);
+  return bal_eval<F>(gathered, nr, nr, out, s);
+}
+
+}  // namespace
+}  // namespace nrmf
+
+using namespace nrmf;
+
+extern "C" {
+
+int nrmf_dist_shard(int64_t n_global, int world, int rank, int64_t* offset, int64_t* count) {
+  if (n_global < 0 || world < 1 || rank < 0 || rank >= world || !offset || !count) return NRMF_EINVAL;
+  if (!is_pow2(world)) return NRMF_ESHARD;
+  shard(n_global, world, rank, offset, count);
+  return NRMF_OK;
+}
+
+size_t nrmf_dist_workspace_bytes(int64_t n_global, int world, int elem_bytes) {
+  if (n_global < 0 || world < 1 || (elem_bytes != 4 && elem_bytes != 8)) return 0;
+  return dist_ws(n_global, world, (size_t)elem_bytes);
+}
+
+int nrmf_dist_d(int64_t n_global, int64_t offset, int64_t count, const double* x_local, double* out,
+                void* ws, size_t ws_bytes, void* nccl_comm, void* stream) {
+  return dist_impl<double>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream);
+}
+int nrmf_dist_s(int64_t n_global, int64_t offset, int64_t count, const float* x_local, float* out,
+                void* ws, size_t ws_bytes, void* nccl_comm, void* stream) {
+  return dist_impl<float>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream);
+}
+
+int nrmf_nccl_unique_id(char* id128) {
+  const NcclApi* api = nccl();
+  if (api == nullptr) return NRMF_ENCCL;
+  if (id128 == nullptr) return NRMF_EINVAL;
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return NRMF_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id128, &id, sizeof id);
+  return NRMF_OK;
+}
+
+int nrmf_nccl_comm_init(int world, int rank, const char* id128, void** comm) {
+  const NcclApi* api = nccl();
+  if (api == nullptr) return NRMF_ENCCL;
+  if (id128 == nullptr || comm == nullptr || world < 1 || rank < 0 || rank >= world) return NRMF_EINVAL;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t c = nullptr;
+  if (api->CommInitRank(&c, world, id, rank) != ncclSuccess) return NRMF_ENCCL;
+  *comm = c;
+  return NRMF_OK;
+}
+
+int nrmf_nccl_comm_destroy(void* comm) {
+  const NcclApi* api = nccl();
+  if (api == nullptr) return NRMF_ENCCL;
+  if (comm == nullptr) return NRMF_EINVAL;
+  return api->CommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? NRMF_OK : NRMF_ENCCL;
+}
+
+}  // extern "C"

@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, bit for bit.
+
+Every expected value comes from ``oracle`` (plain C, same tree) on the same
+seeded inputs; accuracy is checked against the exact reference.  Sizes span
+several tiles/groups and ragged tails; full BASELINE sizes are in the `slow`
+tests at the bottom (same launch configuration bench.py times)."""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import nrmf_inputs as gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+T = 4096
+NP2T = {np.float64: torch.float64, np.float32: torch.float32}
+
+
+@pytest.fixture(scope="module")
+def nrmf():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2509_06220_b200 import _build
+    _build.build()
+    import paper_2509_06220_b200 as m
+    m.lib()
+    torch.cuda.set_device(0)
+    return m
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def bits(v, dt):
+    return np.asarray(v, dtype=dt).tobytes()
+
+
+def gpu_norm(nrmf, x):
+    r = nrmf.norm(dev(x))
+    return r.cpu().numpy()
+
+
+DISTS = {
+    "uniform": lambda s, n, dt: gen.uniform_pm1(s, n, dtype=dt),
+    "normal": lambda s, n, dt: gen.normal(s, n, dtype=dt),
+    "sme": lambda s, n, dt: gen.sme(s, n, dtype=dt),
+}
+
+SIZES = [0, 1, 2, 3, 31, 64, 65, 127, 128, 129, 4095, 4096, 4097, 8191, 2 * T + 3,
+         8 * T - 1, 8 * T, 8 * T + 1, 9 * T + 17, 17 * T, 64 * T + 1, 100 * T + 999, 257 * T + 5]
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("n", SIZES)
+def test_parity_sizes(nrmf, dt, n):
+    x = gen.normal(n + 1, n, dtype=dt)
+    assert bits(gpu_norm(nrmf, x), dt) == bits(oracle.nrmf(x), dt)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("dist", list(DISTS))
+def test_parity_random_sizes(nrmf, dt, dist):
+    rng = np.random.default_rng(12345)
+    for n in rng.integers(1, 1 << 20, 6):
+        x = DISTS[dist](int(n), int(n), dt)
+        assert bits(gpu_norm(nrmf, x), dt) == bits(oracle.nrmf(x), dt), n
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("shift", [1, 2, 3])
+def test_unaligned_base_same_bits(nrmf, dt, shift):
+    """16-byte vector loads vs element loads give identical bits."""
+    n = 37 * T + 11
+    x = gen.uniform_pm1(9, n, dtype=dt)
+    buf = torch.zeros(n + 8, dtype=NP2T[dt], device="cuda")
+    buf[shift:shift + n] = dev(x)
+    view = buf[shift:shift + n]
+    assert view.data_ptr() % 16 != 0 or shift * np.dtype(dt).itemsize % 16 == 0
+    r = nrmf.norm(view).cpu().numpy()
+    assert bits(r, dt) == bits(oracle.nrmf(x), dt)
+
+
+def test_c1_dnrmf_2p20_uniform(nrmf):
+    """BASELINE config C1: DNRMF fp64, n = 2^20, U[-1,1)."""
+    for seed in range(1, 6):
+        x = gen.uniform_pm1(seed, 1 << 20)
+        r = gpu_norm(nrmf, x)
+        assert bits(r, np.float64) == bits(oracle.nrmf(x), np.float64)
+        assert oracle.relerr(r, oracle.exact(x)) < 3
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_reproducible_across_runs_and_grids(nrmf, dt):
+    n = 300 * T + 77
+    x = dev(gen.normal(3, n, dtype=dt))
+    ref = nrmf.norm(x).cpu().numpy()
+    for _ in range(100):
+        assert bits(nrmf.norm(x).cpu().numpy(), dt) == bits(ref, dt)
+    try:
+        for g in (1, 7, 148, 296, 592):
+            nrmf._debug_set_grid(g)
+            assert bits(nrmf.norm(x).cpu().numpy(), dt) == bits(ref, dt), g
+    finally:
+        nrmf._debug_set_grid(0)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_special_values(nrmf, dt):
+    """Non-finite inputs follow Listing 2 literally on both sides (reading R4):
+    inf anywhere -> inf; a NaN collapses to +0 when it meets a +0 leaf."""
+    n = 20 * T + 5
+    rng = np.random.default_rng(4)
+    cases = []
+    x = gen.uniform_pm1(1, n, dtype=dt); x[rng.integers(0, n)] = np.inf; cases.append(x)
+    x = gen.uniform_pm1(2, n, dtype=dt); x[rng.integers(0, n, 5)] = np.nan; cases.append(x)
+    x = gen.uniform_pm1(3, n, dtype=dt); x[-1] = np.nan; cases.append(x)     # NaN in the tail tile
+    x = np.full(n, np.nan, dtype=dt); cases.append(x)
+    x = np.zeros(n, dtype=dt); x[::7] = -0.0; cases.append(x)
+    x = np.zeros(n, dtype=dt); x[rng.integers(0, n, 3)] = [np.inf, -np.inf, np.nan]; cases.append(x)
+    info = np.finfo(dt)
+    x = np.full(n, info.tiny, dtype=dt) * dt(0.5); cases.append(x)            # subnormals
+    x = np.full(n, info.max / 4, dtype=dt); cases.append(x)                   # overflows to inf
+    x = np.zeros(n, dtype=dt); x[0] = info.max; cases.append(x)
+    for x in cases:
+        g, o = gpu_norm(nrmf, x), oracle.nrmf(x)
+        if np.isnan(o):
+            assert np.isnan(g)
+        else:
+            assert bits(g, dt) == bits(o, dt)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_hypot_many_pairs_via_columns(nrmf, dt):
+    """rows = 2 columns: col_norms[j] = v1_hypot(A[0,j], A[1,j]) (the lane tree
+    pads with exact v1(a,0) = a nodes).  10^6 pairs over the full exponent
+    range, subnormals and exact ties, GPU == oracle bit for bit."""
+    m = 1 << 20
+    rng = np.random.default_rng(5)
+    info = np.finfo(dt)
+    emin, emax = (-1074, 1023) if dt == np.float64 else (-149, 127)
+    a = np.ldexp(rng.uniform(1, 2, m), rng.integers(emin, emax, m)).astype(dt)
+    b = np.ldexp(rng.uniform(1, 2, m), rng.integers(emin, emax, m)).astype(dt)
+    k = m // 4
+    b[:k] = (a[:k] * np.ldexp(1.0, rng.integers(-3, 3, k))).astype(dt)   # q near 1
+    a[k:2 * k] = np.ldexp(rng.integers(0, 1 << 20, k), emin).astype(dt)   # subnormals
+    A = np.empty(2 * m, dtype=dt)
+    A[0::2], A[1::2] = a, b
+    col = nrmf.cols(dev(A).as_strided((2, m), (1, 2)), frob=False).cpu().numpy()
+    # a 2-element column is one v1_hypot (two-hot pin of the tree, tests/test_oracle_tree.py)
+    assert col.tobytes() == oracle.v1_hypot_array(a, b).tobytes()
+    sub = 512
+    exp, _ = oracle.cols(A[:2 * sub], 2, sub, 2)
+    assert col[:sub].tobytes() == exp.tobytes()
+    assert math.isfinite(info.max)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("r,c,ld", [(4096, 1000, 4096), (4096, 37, 4100), (1000, 333, 1000),
+                                    (1, 5, 1), (4097, 20, 4097), (9000, 33, 9003), (3 * 4096, 8, 3 * 4096),
+                                    (4096, 1, 4096), (7, 300, 9)])
+def test_cols_parity(nrmf, dt, r, c, ld):
+    A = gen.colscaled_normal(7, r, c, ld=ld, dtype=dt)
+    At = dev(A).as_strided((r, c), (1, ld))
+    col, fr = nrmf.cols(At)
+    ecol, efr = oracle.cols(A, r, c, ld)
+    assert col.cpu().numpy().tobytes() == ecol.tobytes()
+    assert bits(fr.cpu().numpy(), dt) == bits(efr, dt)
+    if r == ld == T:
+        assert bits(fr.cpu().numpy(), dt) == bits(oracle.nrmf(A), dt)
+
+
+def test_cols_empty_shapes(nrmf):
+    for r, c in ((0, 5), (5, 0), (0, 0)):
+        A = torch.zeros(max(r, 1) * max(c, 1), dtype=torch.float64, device="cuda").as_strided((r, c), (1, max(r, 1)))
+        col, fr = nrmf.cols(A)
+        assert col.numel() == c and torch.all(col == 0) and fr.item() == 0
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_complex_view(nrmf, dt):
+    n = 50 * T + 3
+    x = gen.normal(8, 2 * n, dtype=dt)
+    z = dev(x).view(torch.complex128 if dt == np.float64 else torch.complex64)
+    assert bits(nrmf.norm_complex(z).cpu().numpy(), dt) == bits(oracle.nrmf(x), dt)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("n", [0, 5, 4096 * 512, 4096 * 512 * 3 + 17, (1 << 24) + 5])
+def test_host_streaming_same_bits(nrmf, dt, n):
+    x = gen.normal(21, n, dtype=dt)
+    h = torch.from_numpy(x).pin_memory()
+    r = nrmf.norm(h).numpy()
+    assert bits(r, dt) == bits(oracle.nrmf(x), dt)
+
+
+def test_dist_world1(nrmf):
+    """nrmf_dist_d on a 1-rank NCCL communicator equals nrmf_d bitwise."""
+    import torch.distributed as td
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    created = False
+    if not td.is_initialized():
+        td.init_process_group("gloo", rank=0, world_size=1)
+        created = True
+    try:
+        for dt in (np.float64, np.float32):
+            for n in (1, 4097, 100 * T + 5):
+                x = gen.normal(2, n, dtype=dt)
+                r = nrmf.dist(dev(x), n).cpu().numpy()
+                assert bits(r, dt) == bits(oracle.nrmf(x), dt)
+    finally:
+        for c in list(nrmf._comms.values()):
+            c.close()
+        nrmf._comms.clear()
+        if created:
+            td.destroy_process_group()
+
+
+def test_errors_raise(nrmf):
+    with pytest.raises(ValueError):
+        nrmf.norm(torch.zeros(10, dtype=torch.float16, device="cuda"))
+    with pytest.raises(ValueError):
+        nrmf.norm(torch.zeros(10, 10, dtype=torch.float64, device="cuda").t())
+
+
+# ------------------------------------------------------------ full sizes
+@pytest.mark.slow
+def test_c2_snrmf_2p28(nrmf):
+    n = 1 << 28
+    x = gen.sme(1, n)
+    r = gpu_norm(nrmf, x)
+    assert bits(r, np.float32) == bits(oracle.nrmf(x), np.float32)
+    assert oracle.relerr(r, oracle.exact(x), np.float32) <= 64
+
+
+@pytest.mark.slow
+def test_c3_dnrmf_2p30_normal(nrmf):
+    n = 1 << 30
+    x = gen.normal(1, n)
+    r = gpu_norm(nrmf, x)
+    o = oracle.nrmf(x)
+    assert bits(r, np.float64) == bits(o, np.float64)
+    assert oracle.relerr(r, oracle.exact(x)) <= 64
+
+
+@pytest.mark.slow
+def test_c4_cols_4096x65536(nrmf):
+    r, c = 4096, 65536
+    A = gen.colscaled_normal(1, r, c)
+    col, fr = nrmf.cols(dev(A).as_strided((r, c), (1, r)))
+    ecol, efr = oracle.cols(A, r, c, r)
+    assert col.cpu().numpy().tobytes() == ecol.tobytes()
+    assert bits(fr.cpu().numpy(), np.float64) == bits(efr, np.float64)
+    assert oracle.relerr(fr.cpu().numpy(), oracle.exact(A)) <= 64
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("variant", ["lit", "fin", "fin2"])
+def test_c5_extreme_2p27(nrmf, variant):
+    n = 1 << 27
+    x = gen.extreme(1, n, variant)
+    r = gpu_norm(nrmf, x)
+    o = oracle.nrmf(x)
+    assert bits(r, np.float64) == bits(o, np.float64)
+    z = dev(x).view(torch.complex128)
+    assert bits(nrmf.norm_complex(z).cpu().numpy(), np.float64) == bits(o, np.float64)
+    ex = oracle.exact(x)
+    if variant == "lit":
+        assert ex == np.inf and r == np.inf
+    else:
+        assert math.isfinite(ex) and oracle.relerr(r, ex) <= 64
