@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the B200 xNRMF path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c2|c4|c1] [--no-extras]
+
+Default workload (BASELINE.json metric "DNRMF/SNRMF GB/s and % of binding
+roofline at n=2^30; max error (ulp) vs exact", config C3): DNRMF of one fp64
+array of n = 2^30 N(0,1) elements (8 GiB, host Box-Muller, seed 1), sharded
+contiguously over N GPUs (nrmf_dist_d; nrmf_d at N=1).  One step = one full
+xNRMF evaluation of the whole array (all tree levels: loads, lane trees,
+cross-lane, group, grid and rank combine).  Inputs (8 GiB, 1 GiB per GPU at
+N=8) are larger than the 126 MB L2, so no L2 flush is needed.  Timed with
+CUDA events on the launching stream, max over ranks.
+
+Rank 0 prints ONE JSON line.  Extras on the line: roofline (dominant kernel,
+HBM bytes vs MEASURED_PEAKS.json), cpu_baseline (the C oracle on one host
+core, full workload), e2e (host-resident input through nrmf.norm / the
+nrmf_host_d C-ABI call, H2D inside the timed region), accuracy (relerr and
+ulp vs the exact norm, bit-equality with the oracle), the SNRMF n=2^30 point
+the metric also names, clocks sampled with NVML during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DNRMF/SNRMF GB/s and % of binding roofline at n=2^30; max error (ulp) vs exact"
+N_C3 = 1 << 30
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index: int, period: float = 0.01):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.nv = None
+            self.err = str(e)
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ helpers
+def ulp_distance(a: float, b: float, dt) -> int | None:
+    if not (math.isfinite(a) and math.isfinite(b)):
+        return None if a != b else 0
+    ia = np.asarray(a, dtype=dt).view(np.int64 if dt == np.float64 else np.int32).item()
+    ib = np.asarray(b, dtype=dt).view(np.int64 if dt == np.float64 else np.int32).item()
+    return abs(ia - ib)
+
+
+def make_input(config: str, n: int, off: int, dt):
+    import nrmf_inputs as gen
+    if config in ("c3",):
+        return gen.normal(1, n, off, dtype=dt)
+    if config == "c2":
+        return gen.sme(1, n, off, dtype=dt)
+    if config == "c1":
+        return gen.uniform_pm1(1, n, off, dtype=dt)
+    raise ValueError(config)
+
+
+def time_loop(fn, steps: int, stream):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps  # ms per step
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The oracle (plain C, one host core) on the same workload: each step is a
+    bounded contiguous sample of 2^24 elements of the C3 array (offset varies
+    per step), so the run ends within minutes."""
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    dt = np.float64 if args.config in ("c3", "c1", "c4") else np.float32
+    sample = 1 << 24
+    esz = np.dtype(dt).itemsize
+    ts = []
+    for s in range(args.warmup + args.steps):
+        x = make_input(args.config, sample, (s * sample) % N_C3, dt)
+        t0 = time.perf_counter()
+        oracle.nrmf(x)
+        t1 = time.perf_counter()
+        if s >= args.warmup:
+            ts.append(t1 - t0)
+    ms = 1e3 * sum(ts) / len(ts)
+    gbs = sample * esz / (ms * 1e-3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32", "data": "synthetic",
+        "config": {"workload": cfg_name(args.config), "n": N_C3, "sample_per_step": sample},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"2^24 contiguous elements of the {args.config.upper()} array per step"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cfg_name(c):
+    return {"c3": "C3 DNRMF fp64 n=2^30 N(0,1) (nrmf_d / nrmf_dist_d)",
+            "c2": "SNRMF fp32 n=2^30 s*m*2^e e in [-20,20] (nrmf_s)",
+            "c1": "C1 DNRMF fp64 n=2^20 U[-1,1)"}.get(c, c)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as td
+
+    import paper_2509_06220_b200 as nrmf
+    from paper_2509_06220_b200 import _build
+    _build.build()
+    nrmf.lib()
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        td.init_process_group("nccl", device_id=device)
+
+    config = args.config
+    dt = np.float64 if config in ("c3", "c1") else np.float32
+    tdt = torch.float64 if dt == np.float64 else torch.float32
+    esz = np.dtype(dt).itemsize
+    n = N_C3 if config in ("c3", "c2") else (1 << 20)
+    off, cnt = nrmf.shard(n, world, rank) if world > 1 else (0, n)
+
+    t0 = time.time()
+    x_host = torch.empty(cnt, dtype=tdt).pin_memory()
+    import nrmf_inputs as gen
+    xh = x_host.numpy()
+    if config == "c3":
+        gen.normal(1, cnt, off, dtype=dt, out=xh)
+    elif config == "c2":
+        gen.sme(1, cnt, off, dtype=dt, out=xh)
+    else:
+        gen.uniform_pm1(1, cnt, off, dtype=dt, out=xh)
+    x = x_host.to(device)
+    torch.cuda.synchronize()
+    t_gen = time.time() - t0
+
+    stream = torch.cuda.current_stream(device)
+    out = torch.empty((), dtype=tdt, device=device)
+    comm = nrmf.comm_for(None) if world > 1 else None
+
+    if world > 1:
+        def step():
+            nrmf.dist(x, n, comm=comm, out=out)
+        launches_per_step = 2  # tile-tree kernel + rank-tree kernel (the NCCL allgather is NCCL's)
+    else:
+        def step():
+            nrmf.norm(x, out=out)
+        launches_per_step = 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        td.barrier()
+    with ClockSampler(local) as clk:
+        ms = time_loop(step, args.steps, stream)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=device)
+        td.all_reduce(tt, op=td.ReduceOp.MAX)
+        ms = tt.item()
+        td.barrier()
+    result = out.cpu().item()
+
+    # dominant kernel alone (the local tile-tree kernel), same stream, same data
+    if world > 1:
+        kern_ms = time_loop(lambda: nrmf.norm(x, out=out), args.steps, stream)
+    else:
+        kern_ms = ms
+    total_bytes = n * esz
+    gbs = total_bytes / (ms * 1e-3) / 1e9
+
+    peaks, peak_src = load_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    kern_gbs = cnt * esz / (kern_ms * 1e-3) / 1e9
+    clocks = clk.summary()
+
+    line = {
+        "metric": METRIC, "value": round(gbs, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32",
+        "data": "synthetic",
+        "config": {"workload": cfg_name(config), "n": n, "global_batch": n, "elem_bytes": esz,
+                   "parallelism": f"shard{world}", "l2": "input > 126 MB L2 (no flush needed)",
+                   "tree_version": nrmf.tree_version(), "seed": 1},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "elements_per_s": round(n / (ms * 1e-3), 1),
+        "roofline": {"bound": "hbm", "achieved": round(kern_gbs, 2), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(kern_gbs / hbm_peak, 4), "traffic": None,
+                     "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs (copy)",
+                     "kernel": "nrmf_tiles_kernel<double|float,VEC=1>",
+                     "algorithmic_bytes_per_launch": cnt * esz},
+    }
+    if rank == 0:
+        line["result_hex"] = np.asarray(result, dtype=dt).tobytes()[::-1].hex()
+
+    # ---------------- e2e: host-resident input through the public API
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    if world == 1:
+        host_out = torch.empty((), dtype=tdt).pin_memory()
+
+        def e2e_step():
+            nrmf.norm(x_host, out=host_out)          # nrmf_host_d: H2D ring + kernels + D2H
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        e2e_ok = host_out.item() == result or (math.isnan(result) and math.isnan(host_out.item()))
+    else:
+        xdev = torch.empty_like(x)
+
+        def e2e_step():
+            xdev.copy_(x_host, non_blocking=True)
+            nrmf.dist(xdev, n, comm=comm, out=out)
+            return out.cpu()
+        e2e_step()
+        td.barrier()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+        td.all_reduce(tt, op=td.ReduceOp.MAX)
+        e2e_ms = tt.item()
+        e2e_ok = out.cpu().item() == result
+    line["e2e"] = {"value": round(total_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                   "h2d_bytes_per_step": total_bytes, "d2h_bytes_per_step": esz,
+                   "ms_per_step": round(e2e_ms, 3), "steps": e2e_steps, "same_bits": bool(e2e_ok),
+                   "api": "nrmf.norm(pinned host tensor) -> nrmf_host_d" if world == 1 else
+                          "pinned H2D copy + nrmf.dist -> nrmf_dist_d"}
+
+    # ---------------- extras (rank 0, N=1): accuracy, oracle CPU baseline, SNRMF point
+    if rank == 0 and world == 1 and not args.no_extras:
+        import oracle
+        oracle.build()
+        t0 = time.perf_counter()
+        ex = float(oracle.exact(xh))
+        t_exact = time.perf_counter() - t0
+        acc = {"relerr_eps": oracle.relerr(result, ex, dt), "ulp": ulp_distance(result, ex, dt),
+               "exact_hex": np.asarray(ex, dtype=dt).tobytes()[::-1].hex(),
+               "bound_thm3_eps": round(oracle.ub_relerr_H(12 + int(math.log2(max(1, n // 4096))), dt), 3)}
+        t0 = time.perf_counter()
+        o = oracle.nrmf(xh)
+        t_or = time.perf_counter() - t0
+        acc["bit_exact_vs_oracle"] = bool(np.asarray(o, dtype=dt).tobytes() == np.asarray(result, dtype=dt).tobytes())
+        line["accuracy"] = acc
+        line["cpu_baseline"] = {"value": round(total_bytes / t_or / 1e9, 4), "unit": "GB/s", "cores": 1,
+                                "kind": "oracle", "seconds": round(t_or, 3),
+                                "sample": f"full workload ({n} elements), single-threaded C oracle",
+                                "cpu": cpu_model()}
+        line["timing_s"] = {"gen": round(t_gen, 2), "exact": round(t_exact, 2), "oracle": round(t_or, 2)}
+        if config == "c3" and not args.no_snrmf:
+            line["snrmf"] = snrmf_point(nrmf, device, stream, args, hbm_peak)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        comm.close()
+        td.destroy_process_group()
+    return 0
+
+
+def snrmf_point(nrmf, device, stream, args, hbm_peak):
+    """The SNRMF half of the metric: fp32 n = 2^30, C2 recipe (s*m*2^e)."""
+    import torch
+
+    import nrmf_inputs as gen
+    import oracle
+    n = N_C3
+    xh = torch.empty(n, dtype=torch.float32).pin_memory()
+    gen.sme(1, n, 0, dtype=np.float32, out=xh.numpy())
+    x = xh.to(device)
+    out = torch.empty((), dtype=torch.float32, device=device)
+    for _ in range(args.warmup):
+        nrmf.norm(x, out=out)
+    with ClockSampler(device.index) as clk:
+        ms = time_loop(lambda: nrmf.norm(x, out=out), args.steps, stream)
+    r = out.cpu().item()
+    ex = float(oracle.exact(xh.numpy()))
+    gbs = n * 4 / (ms * 1e-3) / 1e9
+    del x
+    return {"workload": "SNRMF fp32 n=2^30 s*m*2^e, e in [-20,20] (C2 recipe)", "value": round(gbs, 2),
+            "unit": "GB/s", "ms_per_step": round(ms, 4),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(gbs / hbm_peak, 4)},
+            "relerr_eps": oracle.relerr(r, ex, np.float32), "ulp": ulp_distance(r, ex, np.float32),
+            "clocks": clk.summary()}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} cpus)"
+    except OSError:
+        pass
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c2", "c1"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-snrmf", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

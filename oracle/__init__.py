@@ -71,6 +71,14 @@ def lib():
         L.oracle_nrmf_cols_d.restype = ctypes.c_int
         L.oracle_nrmf_cols_s.argtypes = [i64, i64, i64, vp, i64, i64, vp, vp]
         L.oracle_nrmf_cols_s.restype = ctypes.c_int
+        for sfx in ("d", "s"):
+            getattr(L, "exact_acc_" + sfx).argtypes = [vp, i64, vp, ip]
+            getattr(L, "exact_acc_" + sfx).restype = None
+            getattr(L, "exact_round_" + sfx).argtypes = [vp, ctypes.c_int]
+            getattr(L, "exact_acc_words_" + sfx).restype = ctypes.c_int
+        L.exact_round_d.restype = d
+        L.exact_round_s.restype = f
+        L.exact_acc_merge.argtypes = [vp, vp, ctypes.c_int]; L.exact_acc_merge.restype = None
         L.exact_nrm_d.argtypes = [vp, i64]; L.exact_nrm_d.restype = d
         L.exact_nrm_s.argtypes = [vp, i64]; L.exact_nrm_s.restype = f
         _lib = L
@@ -217,11 +225,37 @@ def combine_ranks(values):
     return combine(np.array(vals, dtype=type(vals[0])))
 
 
-def exact(x):
-    """RN(sqrt(sum x_i^2)) computed exactly (integer superaccumulator)."""
+def exact(x, threads: int | None = None):
+    """RN(sqrt(sum x_i^2)) computed exactly (integer superaccumulator).
+    Large inputs are accumulated in disjoint chunks on host threads; integer
+    addition is exact and associative, so the result does not depend on it."""
     x = _arr(x)
-    f = lib().exact_nrm_d if _is64(x) else lib().exact_nrm_s
-    return x.dtype.type(f(x.ctypes.data, x.size))
+    L = lib()
+    if threads is None:
+        threads = min(os.cpu_count() or 1, 16) if x.size >= (1 << 22) else 1
+    if threads <= 1:
+        f = L.exact_nrm_d if _is64(x) else L.exact_nrm_s
+        return x.dtype.type(f(x.ctypes.data, x.size))
+    from concurrent.futures import ThreadPoolExecutor
+    sfx = "d" if _is64(x) else "s"
+    words = getattr(L, "exact_acc_words_" + sfx)()
+    acc_f = getattr(L, "exact_acc_" + sfx)
+    bounds = np.linspace(0, x.size, threads + 1).astype(np.int64)
+    accs = [np.zeros(words, dtype=np.uint64) for _ in range(threads)]
+    flags = [ctypes.c_int(0) for _ in range(threads)]
+
+    def work(k):
+        a, b = int(bounds[k]), int(bounds[k + 1])
+        acc_f(x.ctypes.data + a * x.itemsize, b - a, accs[k].ctypes.data, ctypes.byref(flags[k]))
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(threads)))
+    for k in range(1, threads):
+        L.exact_acc_merge(accs[0].ctypes.data, accs[k].ctypes.data, words)
+    fl = 0
+    for v in flags:
+        fl |= v.value
+    return x.dtype.type(getattr(L, "exact_round_" + sfx)(accs[0].ctypes.data, fl))
 
 
 def relerr(r, ref, dtype=np.float64) -> float:

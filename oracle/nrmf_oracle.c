@@ -385,51 +385,87 @@ static double round_sqrt_acc(const uint64_t *acc, int words, int emin, int prec,
     return ldexp((double)(uint64_t)mant, qe);      /* exact: mant <= 2^prec */
 }
 
-double exact_nrm_d(const double *x, int64_t n)
+/* Accumulate sum x_i^2 of x[0..n) into acc (ACC_WORDS_D words, exact);
+ * flags |= 1 for a NaN, |= 2 for an infinity.  Exact integer addition is
+ * associative, so disjoint chunks may be accumulated separately and their
+ * accumulators added (used to spread large inputs over host threads).      */
+void exact_acc_d(const double *x, int64_t n, uint64_t *acc, int *flags)
 {
-    uint64_t acc[ACC_WORDS_D];
-    memset(acc, 0, sizeof acc);
-    int any_nan = 0, any_inf = 0;
     for (int64_t i = 0; i < n; ++i) {
         uint64_t u;
         memcpy(&u, &x[i], 8);
         const int ef = (int)((u >> 52) & 0x7FF);
         const uint64_t fr = u & 0xFFFFFFFFFFFFFULL;
-        if (ef == 0x7FF) { if (fr) any_nan = 1; else any_inf = 1; continue; }
+        if (ef == 0x7FF) { *flags |= fr ? 1 : 2; continue; }
         const uint64_t M = ef ? (fr | (1ULL << 52)) : fr;
         if (!M) continue;
-        /* x = M * 2^(E), E = ef - 1075 (normal) or -1074 (subnormal);
+        /* x = M * 2^E, E = ef - 1075 (normal) or -1074 (subnormal);
            x^2 = M^2 * 2^(2E) = M^2 * 2^(shift) * 2^(-2148). */
         const int E = ef ? (ef - 1075) : -1074;
-        const int shift = 2 * E + 2148;
-        acc_add_shifted(acc, ACC_WORDS_D, (u128)M * M, shift);
+        acc_add_shifted(acc, ACC_WORDS_D, (u128)M * M, 2 * E + 2148);
     }
-    if (any_nan) return NAN;
-    if (any_inf) return INFINITY;
+}
+
+void exact_acc_s(const float *x, int64_t n, uint64_t *acc, int *flags)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t u;
+        memcpy(&u, &x[i], 4);
+        const int ef = (int)((u >> 23) & 0xFF);
+        const uint32_t fr = u & 0x7FFFFFu;
+        if (ef == 0xFF) { *flags |= fr ? 1 : 2; continue; }
+        const uint64_t M = ef ? (fr | (1u << 23)) : fr;
+        if (!M) continue;
+        const int E = ef ? (ef - 150) : -149;
+        acc_add_shifted(acc, ACC_WORDS_S, (u128)M * M, 2 * E + 298);
+    }
+}
+
+/* acc += other (both `words` long) */
+void exact_acc_merge(uint64_t *acc, const uint64_t *other, int words)
+{
+    uint64_t carry = 0;
+    for (int k = 0; k < words; ++k) {
+        u128 s = (u128)acc[k] + other[k] + carry;
+        acc[k] = (uint64_t)s;
+        carry = (uint64_t)(s >> 64);
+    }
+}
+
+double exact_round_d(const uint64_t *acc, int flags)
+{
+    if (flags & 1) return NAN;
+    if (flags & 2) return INFINITY;
     int inf;
     return round_sqrt_acc(acc, ACC_WORDS_D, -1074, 53, 1024, &inf);
+}
+
+float exact_round_s(const uint64_t *acc, int flags)
+{
+    if (flags & 1) return NAN;
+    if (flags & 2) return INFINITY;
+    int inf;
+    double r = round_sqrt_acc(acc, ACC_WORDS_S, -149, 24, 128, &inf);
+    return inf ? INFINITY : (float)r;   /* r is already a float value: exact */
+}
+
+int exact_acc_words_d(void) { return ACC_WORDS_D; }
+int exact_acc_words_s(void) { return ACC_WORDS_S; }
+
+double exact_nrm_d(const double *x, int64_t n)
+{
+    uint64_t acc[ACC_WORDS_D];
+    memset(acc, 0, sizeof acc);
+    int flags = 0;
+    exact_acc_d(x, n, acc, &flags);
+    return exact_round_d(acc, flags);
 }
 
 float exact_nrm_s(const float *x, int64_t n)
 {
     uint64_t acc[ACC_WORDS_S];
     memset(acc, 0, sizeof acc);
-    int any_nan = 0, any_inf = 0;
-    for (int64_t i = 0; i < n; ++i) {
-        uint32_t u;
-        memcpy(&u, &x[i], 4);
-        const int ef = (int)((u >> 23) & 0xFF);
-        const uint32_t fr = u & 0x7FFFFFu;
-        if (ef == 0xFF) { if (fr) any_nan = 1; else any_inf = 1; continue; }
-        const uint64_t M = ef ? (fr | (1u << 23)) : fr;
-        if (!M) continue;
-        const int E = ef ? (ef - 150) : -149;
-        const int shift = 2 * E + 298;
-        acc_add_shifted(acc, ACC_WORDS_S, (u128)M * M, shift);
-    }
-    if (any_nan) return NAN;
-    if (any_inf) return INFINITY;
-    int inf;
-    double r = round_sqrt_acc(acc, ACC_WORDS_S, -149, 24, 128, &inf);
-    return inf ? INFINITY : (float)r;   /* r is already a float value: exact */
+    int flags = 0;
+    exact_acc_s(x, n, acc, &flags);
+    return exact_round_s(acc, flags);
 }

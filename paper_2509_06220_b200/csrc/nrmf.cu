@@ -59,9 +59,9 @@ __global__ void __launch_bounds__(kThreads, 2) nrmf_tiles_kernel(const TileJob<F
       const int64_t rem = job.len - tt * (int64_t)kTile;
       const int valid = rem < kTile ? (int)rem : kTile;
       if (valid == kTile) {
-        tv = VEC ? warp_tile<F, kVec>(tb, kTile) : warp_tile<F, kScalar>(tb, kTile);
+        tv = VEC ? warp_tile<F, kVec>(tb) : warp_tile<F, kScalar>(tb);
       } else {
-        tv = warp_tile<F, kPred>(tb, valid);
+        tv = warp_tile_exact<F, kPred>(tb, valid);
       }
       if (job.tile_out != nullptr && lane == 0) job.tile_out[tau] = tv;
     }
