@@ -25,75 +25,278 @@
 namespace nrmf {
 
 // ------------------------------------------------------------------ kernels
+constexpr int kMaxSteps = 8;
+#ifndef NRMF_STAGES
+#define NRMF_STAGES 2         // TMA ring depth per warp (batches of 4 KiB)
+#endif
+#ifndef NRMF_BPI
+#define NRMF_BPI 1            // batches per loop iteration on the TMA path
+#endif
+#ifndef NRMF_USE_TMA
+#define NRMF_USE_TMA 1        // 0: aligned full tiles use direct LDG.128 instead of the TMA ring
+#endif
+#ifndef NRMF_MIN_BLOCKS
+#define NRMF_MIN_BLOCKS 2     // CTAs per SM the register allocation must allow
+#endif
+constexpr int kStages = NRMF_STAGES;
+constexpr int kBPI = NRMF_BPI;
+static_assert(kStages >= kBPI, "the ring must hold one iteration");
+
+// One evaluation of the tile tree.  Work unit of a warp: a "warp group" of
+// 2^g0 consecutive tiles (an aligned subtree: its first g0 levels are
+// combined in registers); above it, steps of up to 6 levels (fan-in 64) are
+// combined by the last-arriving warp of each group (integer counters in the
+// workspace).  The shape of the tree never depends on g0, the grid or timing.
 template <typename F>
-struct TileJob {
+struct TreeJob {
   const F* x;          // base pointer
   int64_t n_items;     // tiles that contain data
   int64_t tpc;         // tiles per column (vector mode: n_items)
-  int64_t ld;          // elements between column bases (vector mode: unused)
+  int64_t ld;          // elements between column bases (vector mode: 0)
   int64_t len;         // column length (vector mode: n)
-  int64_t p2;          // tiles of the (sub)tree evaluated: power of two >= n_items
-  F* tile_out;         // optional per-tile values
-  F* partials;         // group partials (workspace)
-  unsigned* ticket;    // last-CTA ticket (workspace)
-  F* out;              // result (root of the p2-tile tree); unused if !combine
+  F* tile_out;         // optional: every tile value (column norms)
+  F* vals;             // workspace: warp-group values and higher levels
+  unsigned* cnt;       // workspace: arrival counters of every step (zero between calls)
+  F* out;              // root of the tree; unused if !combine
   int combine;         // 0: only write tile values
+  int g0;              // tile-tree levels combined inside a warp group (<= 3)
+  int nsteps;          // combine steps above the warp groups
+  int lg_fan[kMaxSteps];
+  int64_t nin[kMaxSteps];      // real (non-padding) inputs of step k (nin[0] = warp groups)
+  int64_t val_off[kMaxSteps];  // vals offset of the inputs of step k
+  int64_t cnt_off[kMaxSteps];  // cnt offset of the counters of step k
 };
 
-template <typename F, bool VEC>
-__global__ void __launch_bounds__(kThreads, 2) nrmf_tiles_kernel(const TileJob<F> job) {
-  __shared__ F s_tile[kWarps];
-  __shared__ int s_last;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t n_groups = (job.n_items + kWarps - 1) / kWarps;
-  const int lgp2 = ilog2_64(job.p2);
-  const int glevels = lgp2 < 3 ? lgp2 : 3;
-  const int64_t pg = job.p2 >= kWarps ? job.p2 / kWarps : 1;
+// One warp evaluates the balanced tree over 2^f (<= 64) consecutive values
+// vals[base ..] (entries >= nvals are +0).  All lanes return the value.
+template <typename F>
+__device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_t base, int f) {
+  const int lane = threadIdx.x & 31;
+  F v;
+  int lv;
+  if (f == 6) {
+    const int64_t i = base + 2 * lane;
+    const F a = i < nvals ? __ldcg(vals + i) : F(0);
+    const F b = i + 1 < nvals ? __ldcg(vals + i + 1) : F(0);
+    v = v1h(a, b);
+    lv = 5;
+  } else {
+    const int64_t i = base + lane;
+    v = (lane < (1 << f) && i < nvals) ? __ldcg(vals + i) : F(0);
+    lv = f;
+  }
+  for (int l = 0; l < lv; ++l) v = v1h(v, __shfl_xor_sync(0xffffffffu, v, 1 << l));
+  return v;
+}
 
-  for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
-    const int64_t tau = g * kWarps + w;
-    F tv = F(0);
-    if (tau < job.n_items) {
-      const int64_t col = tau / job.tpc, tt = tau - col * job.tpc;
-      const F* tb = job.x + col * job.ld + tt * (int64_t)kTile;
-      const int64_t rem = job.len - tt * (int64_t)kTile;
-      const int valid = rem < kTile ? (int)rem : kTile;
-      if (valid == kTile) {
-        tv = VEC ? warp_tile<F, kVec>(tb) : warp_tile<F, kScalar>(tb);
-      } else {
-        tv = warp_tile_exact<F, kPred>(tb, valid);
+__device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Node `idx` of step-k input level has been stored by lane 0 and announced
+// with counter value `old`.  If this warp was the last arrival of its group,
+// evaluate the group's subtree and climb.  Last-arriver combine: who computes
+// a node depends on timing, what is computed never does.
+template <typename F>
+__device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    const int f = job.lg_fan[k];
+    const int64_t g = idx >> f;
+    const int64_t fan = int64_t(1) << f;
+    const int64_t rem = job.nin[k] - g * fan;
+    const unsigned expect = (unsigned)(rem < fan ? rem : fan);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != expect - 1) return;
+    __threadfence();  // acquire: the other arrivals' values are visible
+    if (lane == 0) job.cnt[job.cnt_off[k] + g] = 0u;  // ready for the next call
+    const F v = warp_group_bal(job.vals + job.val_off[k], job.nin[k], g * fan, f);
+    if (k + 1 == job.nsteps) {
+      if (lane == 0) *job.out = v;
+      return;
+    }
+    if (lane == 0) {
+      job.vals[job.val_off[k + 1] + g] = v;
+      old = atom_add_release(job.cnt + job.cnt_off[k + 1] + (g >> job.lg_fan[k + 1]), 1u);
+    }
+    ++k;
+    idx = g;
+  }
+}
+
+// Tile tau -> (base pointer, full?).  One 64-bit division per tile at most.
+template <typename F>
+__device__ __forceinline__ bool tile_at(const TreeJob<F>& job, int64_t tau, const F*& base, int64_t& remv) {
+  const int64_t col = job.tpc == 1 ? tau : tau / job.tpc;
+  const int64_t tt = tau - col * job.tpc;
+  base = job.x + col * job.ld + tt * (int64_t)kTile;
+  remv = job.len - tt * (int64_t)kTile;
+  return remv >= kTile;
+}
+
+// SMEM-ring loader: the batches of the warp's full tiles, in the order the
+// warp visits them, arrive by TMA bulk copy (cp.async.bulk, mbarrier
+// complete_tx); kBPI batches are consumed per loop iteration.
+template <typename F>
+struct PipeLoader {
+  static constexpr int BPI = kBPI;
+  static constexpr bool kMaybePadding = false;
+  __device__ __forceinline__ bool all_padding(int) const { return false; }
+
+  const unsigned char* ring;  // this warp's kStages x 4 KiB
+  uint32_t ring_s, bar_s;     // shared-window addresses of ring and barriers
+  uint32_t consumed, issued;  // batches consumed / issued (warp-uniform)
+  int64_t p_grp;              // producer: warp group of the next tile to load
+  int p_k;                    // producer: tile index within that group
+  int p_b;                    // producer: batch index within that tile
+  const F* p_base;            // producer: base of that tile
+  int64_t W;                  // warp-group stride of this warp
+  int G;                      // tiles per warp group
+  int64_t n_groups;
+  uint64_t policy;
+  const TreeJob<F>* job;
+
+  // advance the producer to the next full tile at or after (p_grp, p_k)
+  __device__ __forceinline__ void seek_full() {
+    while (p_grp < n_groups) {
+      const int64_t tau = p_grp * G + p_k;
+      int64_t remv;
+      if (tau < job->n_items && tile_at(*job, tau, p_base, remv)) return;
+      if (++p_k == G) {
+        p_k = 0;
+        p_grp += W;
       }
-      if (job.tile_out != nullptr && lane == 0) job.tile_out[tau] = tv;
+    }
+  }
+  __device__ __forceinline__ void issue() {
+    if (p_grp >= n_groups) return;
+    const uint32_t s = issued % kStages;
+    if ((threadIdx.x & 31) == 0)
+      bulk_load(ring_s + s * kBatchBytes, p_base + (int64_t)p_b * kBatch * Cfg<F>::LANES, kBatchBytes,
+                bar_s + s * 8, policy);
+    ++issued;
+    if (++p_b == Cfg<F>::J / kBatch) {
+      p_b = 0;
+      if (++p_k == G) {
+        p_k = 0;
+        p_grp += W;
+      }
+      seek_full();
+    }
+  }
+  __device__ __forceinline__ void load(int, F (&u)[kBatch * kBPI][Cfg<F>::V]) {
+    constexpr int V = Cfg<F>::V;
+#pragma unroll
+    for (int q = 0; q < kBPI; ++q) {
+      const uint32_t c = consumed + q;
+      const uint32_t s = c % kStages;
+      mbar_wait(bar_s + s * 8, (c / kStages) & 1);
+      const unsigned char* buf = ring + s * kBatchBytes + (threadIdx.x & 31) * 16;
+#pragma unroll
+      for (int r = 0; r < kBatch; ++r) {
+        const unsigned char* src = buf + r * (kBatchBytes / kBatch);
+        if constexpr (V == 2) {
+          const double2 d = *reinterpret_cast<const double2*>(src);
+          u[q * kBatch + r][0] = d.x;
+          u[q * kBatch + r][1] = d.y;
+        } else {
+          const float4 d = *reinterpret_cast<const float4*>(src);
+          u[q * kBatch + r][0] = d.x;
+          u[q * kBatch + r][1] = d.y;
+          u[q * kBatch + r][2] = d.z;
+          u[q * kBatch + r][3] = d.w;
+        }
+      }
+    }
+    __syncwarp();  // every lane holds its values: the stages may be refilled
+    consumed += kBPI;
+#pragma unroll
+    for (int q = 0; q < kBPI; ++q) issue();
+  }
+};
+
+template <typename F, bool TMA>
+__global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(const TreeJob<F> job) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr bool kPipe = TMA && NRMF_USE_TMA;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + w;
+  const int G = 1 << job.g0;
+  const int64_t n_groups = (job.n_items + G - 1) >> job.g0;
+
+  PipeLoader<F> pl;
+  if (kPipe) {
+    pl.ring = smem + w * (kStages * kBatchBytes);
+    pl.ring_s = smem_u32(pl.ring);
+    pl.bar_s = smem_u32(smem + kWarps * kStages * kBatchBytes) + w * kStages * 8;
+    if (lane == 0) {
+      for (int st = 0; st < kStages; ++st) mbar_init(pl.bar_s + st * 8, 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+    pl.consumed = pl.issued = 0;
+    pl.p_grp = gw;
+    pl.p_k = pl.p_b = 0;
+    pl.W = W;
+    pl.G = G;
+    pl.n_groups = n_groups;
+    pl.policy = policy_evict_first();
+    pl.job = &job;
+    pl.seek_full();
+    for (int st = 0; st < kStages; ++st) pl.issue();
+  }
+
+  int64_t pend_idx = -1;
+  unsigned pend_old = 0;
+  for (int64_t grp = gw; grp < n_groups; grp += W) {
+    F s0[1], s1[1], s2[1], gv[1];
+    for (int k = 0; k < G; ++k) {  // rolled
+      const int64_t tau = grp * G + k;
+      F tv = F(0);  // padding tile beyond the data: its subtree is +0
+      if (tau < job.n_items) {
+        const F* tb;
+        int64_t remv;
+        if (tile_at(job, tau, tb, remv)) {
+          if (kPipe) {
+            NodeFast node;
+            tv = warp_tile_impl<F>(pl, node);
+            if (__any_sync(0xffffffffu, node.bad) || tv != tv) tv = warp_tile_exact<F, kVec>(tb, kTile);
+          } else if (TMA) {
+            tv = warp_tile<F, kVec>(tb);
+          } else {
+            tv = warp_tile<F, kScalar>(tb);
+          }
+        } else {
+          tv = warp_tile_exact<F, kPred>(tb, (int)remv);
+        }
+        if (job.tile_out != nullptr && lane == 0) job.tile_out[tau] = tv;
+      }
+      gv[0] = tv;
+      NodeExact ne;
+      if (G == 8) counter_merge<F, 1, 8>(k, gv, s0, s1, s2, ne);
+      else if (G == 4) counter_merge<F, 1, 4>(k, gv, s0, s1, s2, ne);
+      else if (G == 2) counter_merge<F, 1, 2>(k, gv, s0, s1, s2, ne);
     }
     if (!job.combine) continue;
-    if (lane == 0) s_tile[w] = tv;
-    __syncthreads();
-    if (w == 0) {
-      F v = lane < kWarps ? s_tile[lane] : F(0);
-      for (int l = 0; l < glevels; ++l) v = v1h(v, __shfl_xor_sync(0xffffffffu, v, 1 << l));
-      if (lane == 0) {
-        if (pg == 1) *job.out = v;
-        else job.partials[g] = v;
-      }
+    if (job.nsteps == 0) {  // the warp group is the whole tree
+      if (lane == 0) *job.out = gv[0];
+      continue;
     }
-    __syncthreads();
+    // announce this warp group (the counter result is consumed one group
+    // later, so the atomic's round trip overlaps the next group's arithmetic)
+    unsigned old = 0;
+    if (lane == 0) {
+      job.vals[job.val_off[0] + grp] = gv[0];
+      old = atom_add_release(job.cnt + job.cnt_off[0] + (grp >> job.lg_fan[0]), 1u);
+    }
+    if (pend_idx >= 0) climb(job, 0, pend_idx, pend_old);
+    pend_idx = grp;
+    pend_old = old;
   }
-  if (!job.combine || pg == 1) return;
-
-  // deterministic grid combine: last CTA evaluates the top of the tree
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(job.ticket, 1u);
-    s_last = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const F v = block_bal(job.partials, n_groups, pg);
-  if (threadIdx.x == 0) {
-    *job.out = v;
-    *job.ticket = 0u;  // ready for the next call on this workspace
-  }
+  if (pend_idx >= 0) climb(job, 0, pend_idx, pend_old);
 }
 
 // Balanced tree over vals[0..P) (entries >= nvals are +0) -> *out.  One CTA.
@@ -173,13 +376,68 @@ static int device_sms() {
   return cached[dev];
 }
 
-template <typename F, bool VEC>
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Plan of the combine over p2 tiles of which n_items are real: g0 levels
+// inside each warp group, then steps of up to 6 levels (fan-in 64).
+struct Plan {
+  int g0 = 0;
+  int nsteps = 0;
+  int lg_fan[kMaxSteps] = {};
+  int64_t nin[kMaxSteps] = {};
+  int64_t val_off[kMaxSteps] = {};
+  int64_t cnt_off[kMaxSteps] = {};
+  int64_t n_vals = 0;
+  int64_t n_cnt = 0;
+};
+
+static Plan make_plan(int64_t n_items, int64_t p2, int g0_max) {
+  Plan pl;
+  int L = 0;
+  while ((int64_t(1) << L) < p2) ++L;
+  pl.g0 = L < g0_max ? L : g0_max;
+  L -= pl.g0;
+  int64_t nin = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
+  int64_t voff = 0, coff = 0;
+  while (L > 0) {
+    const int f = L < 6 ? L : 6;
+    const int k = pl.nsteps++;
+    pl.lg_fan[k] = f;
+    pl.nin[k] = nin;
+    pl.cnt_off[k] = coff;
+    pl.val_off[k] = voff;
+    const int64_t groups = (nin + (int64_t(1) << f) - 1) >> f;
+    coff += groups;
+    voff += nin;
+    nin = groups;
+    L -= f;
+  }
+  pl.n_vals = voff;
+  pl.n_cnt = coff;
+  return pl;
+}
+
+// Workspace of one tree evaluation: [counters][values] (worst case g0 = 0)
+static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
+  const Plan pl = make_plan(n_items, p2, 0);
+  return align_up((size_t)pl.n_cnt * 4, 256) + align_up((size_t)pl.n_vals * esz, 256) + 256;
+}
+
+template <typename F, bool TMA>
+static size_t kernel_smem() {
+  return (TMA && NRMF_USE_TMA) ? (size_t)kWarps * kStages * kBatchBytes + (size_t)kWarps * kStages * 8 : 0;
+}
+
+template <typename F, bool TMA>
 static int blocks_per_sm() {
   static int cached = 0;
   if (cached == 0) {
+    const size_t sm = kernel_smem<F, TMA>();
+    if (sm > 48 * 1024)
+      cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tiles_kernel<F, VEC>, kThreads, 0) !=
-            cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA>, kThreads, sm) != cudaSuccess ||
         b < 1)
       b = 1;
     cached = b;
@@ -187,34 +445,52 @@ static int blocks_per_sm() {
   return cached;
 }
 
-static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+static int g_grid_override = 0;  // test hook: force a grid size (0 = automatic)
 
-// Workspace layout for one tile-tree evaluation: [ticket: 256 B][partials]
-static size_t tree_ws_bytes(int64_t p2, size_t esz) {
-  const int64_t pg = p2 >= kWarps ? p2 / kWarps : 1;
-  return 256 + align_up((size_t)pg * esz, 256);
-}
-
+// Launch the tree kernel over items (tiles) with mapping (tpc, ld, len).
 template <typename F>
-static int launch_tree(const TileJob<F>& job_in, bool vec, cudaStream_t s, int grid_override) {
-  TileJob<F> job = job_in;
-  const int64_t n_groups = (job.n_items + kWarps - 1) / kWarps;
-  if (n_groups == 0) return NRMF_OK;
+static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int64_t len, int64_t p2,
+                       F* tile_out, F* out, int combine, void* ws, size_t ws_bytes, bool vec,
+                       cudaStream_t s) {
+  if (n_items == 0) return NRMF_OK;
   int64_t grid = (int64_t)device_sms() * (vec ? blocks_per_sm<F, true>() : blocks_per_sm<F, false>());
-  if (grid_override > 0) grid = grid_override;
-  grid = std::min<int64_t>(grid, n_groups);
+  if (g_grid_override > 0) grid = g_grid_override;
+  // warp groups of 8 tiles when there is enough work for every warp
+  const int g0_max = n_items >= 8 * grid * kWarps ? 3 : 0;
+  const Plan pl = combine ? make_plan(n_items, p2, g0_max) : make_plan(n_items, 1, 0);
+  const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
+  const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
+  if (combine && ws_bytes < need) return NRMF_EWORKSPACE;
+  TreeJob<F> job;
+  job.x = x;
+  job.n_items = n_items;
+  job.tpc = tpc;
+  job.ld = ld;
+  job.len = len;
+  job.tile_out = tile_out;
+  job.cnt = reinterpret_cast<unsigned*>(ws);
+  job.vals = reinterpret_cast<F*>(static_cast<char*>(ws) + cnt_bytes);
+  job.out = out;
+  job.combine = combine;
+  job.g0 = pl.g0;
+  job.nsteps = pl.nsteps;
+  for (int k = 0; k < kMaxSteps; ++k) {
+    job.lg_fan[k] = pl.lg_fan[k];
+    job.nin[k] = pl.nin[k];
+    job.val_off[k] = pl.val_off[k];
+    job.cnt_off[k] = pl.cnt_off[k];
+  }
+  const int64_t n_groups = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
+  grid = std::min<int64_t>(grid, (n_groups + kWarps - 1) / kWarps);
   if (vec)
-    nrmf_tiles_kernel<F, true><<<(unsigned)grid, kThreads, 0, s>>>(job);
+    nrmf_tree_kernel<F, true><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
   else
-    nrmf_tiles_kernel<F, false><<<(unsigned)grid, kThreads, 0, s>>>(job);
+    nrmf_tree_kernel<F, false><<<(unsigned)grid, kThreads, kernel_smem<F, false>(), s>>>(job);
   return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
 }
 
-static int g_grid_override = 0;  // test hook: force a grid size (0 = auto)
-
 template <typename F>
-int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes,
-              cudaStream_t s) {
+int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes, cudaStream_t s) {
   // Evaluate the balanced tree over p2 tiles (p2 >= ceil(n/T), power of two)
   // of x[0..n) padded with +0; *out = root.  Caller validated arguments.
   const int64_t nt = (n + kTile - 1) / kTile;
@@ -222,21 +498,8 @@ int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_byt
     if (cudaMemsetAsync(out, 0, sizeof(F), s) != cudaSuccess) return NRMF_ECUDA;
     return NRMF_OK;
   }
-  if (ws_bytes < tree_ws_bytes(p2, sizeof(F))) return NRMF_EWORKSPACE;
-  TileJob<F> job;
-  job.x = x;
-  job.n_items = nt;
-  job.tpc = nt;
-  job.ld = 0;
-  job.len = n;
-  job.p2 = p2;
-  job.tile_out = nullptr;
-  job.ticket = reinterpret_cast<unsigned*>(ws);
-  job.partials = reinterpret_cast<F*>(static_cast<char*>(ws) + 256);
-  job.out = out;
-  job.combine = 1;
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
-  return launch_tree(job, vec, s, g_grid_override);
+  return launch_tree<F>(x, nt, nt, 0, n, p2, nullptr, out, 1, ws, ws_bytes, vec, s);
 }
 
 template int tree_eval<double>(int64_t, const double*, int64_t, double*, void*, size_t, cudaStream_t);
@@ -250,7 +513,7 @@ int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s) {
 template int bal_eval<double>(const double*, int64_t, int64_t, double*, cudaStream_t);
 template int bal_eval<float>(const float*, int64_t, int64_t, float*, cudaStream_t);
 
-size_t tree_workspace(int64_t p2, size_t esz) { return tree_ws_bytes(p2, esz); }
+size_t tree_workspace(int64_t p2, size_t esz) { return tree_ws_bytes(p2, p2, esz); }
 
 // ---------------------------------------------------------------- vector
 template <typename F>
@@ -265,15 +528,16 @@ static int nrmf_vec(int64_t n, const F* x, F* out, void* ws, size_t ws_bytes, vo
 }
 
 // ---------------------------------------------------------------- columns
-// Workspace: [ticket 256][tile values: cols*tpc if tpc>1][partials]
+// rows <= T: one tile per column, the tree kernel writes col_norms (its tile
+// values) and combines them into frob.  rows > T: tile values into the
+// workspace, then per-column trees and the frob tree (cols_combine_kernel).
+// Workspace (rows > T): [ticket 256][tile values cols*tpc][block partials]
 static size_t cols_ws_bytes(int64_t rows, int64_t cols, size_t esz) {
   const int64_t tpc = std::max<int64_t>((rows + kTile - 1) / kTile, 1);
   const int64_t p2cols = pow2_ceil(std::max<int64_t>(cols, 1));
-  size_t b = 256;
-  if (tpc > 1) b += align_up((size_t)(cols * tpc) * esz, 256);
+  if (tpc == 1) return tree_ws_bytes(std::max<int64_t>(cols, 1), p2cols, esz);
   const int64_t nblk = (cols + kThreads - 1) / kThreads;
-  b += align_up((size_t)std::max<int64_t>({p2cols / kWarps, nblk, 1}) * esz, 256);
-  return b;
+  return 256 + align_up((size_t)(cols * tpc) * esz, 256) + align_up((size_t)std::max<int64_t>(nblk, 1) * esz, 256);
 }
 
 template <typename F>
@@ -298,35 +562,15 @@ static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F*
   if (ws_bytes < cols_ws_bytes(rows, cols, sizeof(F))) return NRMF_EWORKSPACE;
   const int64_t tpc = (rows + kTile - 1) / kTile;
   const int64_t p2cols = pow2_ceil(cols);
+  const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && ((ld * (int64_t)sizeof(F)) & 15) == 0;
+  if (tpc == 1)
+    return launch_tree<F>(A, cols, 1, ld, rows, p2cols, col_norms, frob, frob != nullptr ? 1 : 0, ws, ws_bytes,
+                          vec, s);
   unsigned* ticket = reinterpret_cast<unsigned*>(ws);
   char* base = static_cast<char*>(ws) + 256;
-  const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && ((ld * (int64_t)sizeof(F)) & 15) == 0;
-  TileJob<F> job;
-  job.x = A;
-  job.tpc = tpc;
-  job.ld = ld;
-  job.len = rows;
-  job.ticket = ticket;
-  if (tpc == 1) {
-    // one tile per column: tile value = column norm; frob = tree over columns
-    job.n_items = cols;
-    job.p2 = p2cols;
-    job.tile_out = col_norms;
-    job.partials = reinterpret_cast<F*>(base);
-    job.out = frob;
-    job.combine = frob != nullptr ? 1 : 0;
-    return launch_tree(job, vec, s, g_grid_override);
-  }
-  // multi-tile columns: tile values, then per-column trees + frob tree
   F* vals = reinterpret_cast<F*>(base);
   F* partials = reinterpret_cast<F*>(base + align_up((size_t)(cols * tpc) * sizeof(F), 256));
-  job.n_items = cols * tpc;
-  job.p2 = 1;
-  job.tile_out = vals;
-  job.partials = nullptr;
-  job.out = nullptr;
-  job.combine = 0;
-  int st = launch_tree(job, vec, s, g_grid_override);
+  int st = launch_tree<F>(A, cols * tpc, tpc, ld, rows, 1, vals, nullptr, 0, ws, ws_bytes, vec, s);
   if (st != NRMF_OK) return st;
   const int64_t nblk = (cols + kThreads - 1) / kThreads;
   cols_combine_kernel<F><<<(unsigned)nblk, kThreads, 0, s>>>(vals, cols, tpc, pow2_ceil(tpc), col_norms,
@@ -373,7 +617,7 @@ static size_t host_ws_bytes(int64_t n, size_t esz) {
   const int64_t p2 = pow2_ceil(nt);
   const int64_t c = std::min<int64_t>(p2, kChunkTiles);
   const int64_t nchunks = (nt + c - 1) / c;
-  return tree_ws_bytes(c, esz) + align_up((size_t)nchunks * esz, 256) + 256 +
+  return tree_ws_bytes(c, c, esz) + align_up((size_t)nchunks * esz, 256) + 256 +
          (size_t)kRing * (size_t)(c * kTile) * esz;
 }
 
@@ -390,7 +634,7 @@ static int nrmf_host_impl(int64_t n, const F* host_x, F* host_out, void* ws, siz
   const int64_t nchunks = (nt + c - 1) / c;
   char* p = static_cast<char*>(ws);
   void* tree_ws = p;
-  const size_t tws = tree_ws_bytes(c, sizeof(F));
+  const size_t tws = tree_ws_bytes(c, c, sizeof(F));
   p += tws;
   F* chunk_vals = reinterpret_cast<F*>(p);
   p += align_up((size_t)nchunks * sizeof(F), 256);
@@ -473,7 +717,7 @@ int nrmf_tree_params(int elem_bytes, int* lanes, int* J, int* tile) {
 size_t nrmf_workspace_bytes(int64_t n, int elem_bytes) {
   if (n < 0 || (elem_bytes != 4 && elem_bytes != 8)) return 0;
   const int64_t nt = std::max<int64_t>((n + kTile - 1) / kTile, 1);
-  return tree_ws_bytes(pow2_ceil(nt), (size_t)elem_bytes);
+  return tree_ws_bytes(nt, pow2_ceil(nt), (size_t)elem_bytes);
 }
 
 int nrmf_d(int64_t n, const double* x, double* out, void* ws, size_t ws_bytes, void* stream) {

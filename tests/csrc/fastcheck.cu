@@ -1,0 +1,152 @@
+// tests/csrc/fastcheck.cu -- GPU unit check of the fast node sequences
+// (nrmf_device.cuh: fast_div_n / fast_sqrt_n / v1h_fast_n) against the CUDA
+// IEEE-correct intrinsics (__ddiv_rn, __dsqrt_rn, __fdiv_rn, __fsqrt_rn) and
+// the exact-intrinsic node v1h.  Test infrastructure; built by the test.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "../../paper_2509_06220_b200/csrc/nrmf_device.cuh"
+using namespace nrmf;
+
+__device__ __forceinline__ uint64_t mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+struct Counts {
+  unsigned long long checked, fast, mism;
+};
+
+__device__ double gen_d(uint64_t k, int mode) {
+  const uint64_t k2 = mix(k);
+  int e;
+  if (mode == 0) e = (int)(k2 % 2098) - 1074;        // full range incl. subnormals
+  else e = (int)(k2 % 61) - 30;                     // moderate
+  double v = ldexp(1.0 + (double)(k >> 12) * 0x1p-52, e);
+  return (k & 1) ? -v : v;
+}
+
+// pairs: y = x * 2^d * (1 + small) with d small (q near 1) or arbitrary
+__global__ void check_node_d(uint64_t seed, uint64_t n, int mode, Counts* c) {
+  unsigned long long ck = 0, fa = 0, mi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    const double x = gen_d(k, mode);
+    double y;
+    if (mix(k + 7) & 1) y = gen_d(mix(k + 3), mode);
+    else y = ldexp(1.0 + (double)(mix(k + 5) >> 12) * 0x1p-52, ilogb(x) - (int)(mix(k + 9) % 4)) * ((k & 2) ? -1 : 1);
+    bool bad = false;
+    const double h = v1h_fast<true>(x, y, bad);
+    const double e = v1h(x, y);
+    ++ck;
+    if (!bad) {
+      ++fa;
+      if (__double_as_longlong(h) != __double_as_longlong(e)) ++mi;
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
+}
+
+__global__ void check_node_s(uint64_t seed, uint64_t n, int mode, Counts* c) {
+  unsigned long long ck = 0, fa = 0, mi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    const int e1 = mode == 0 ? (int)(mix(k) % 277) - 149 : (int)(mix(k) % 41) - 20;
+    const float x = ldexpf(1.0f + (float)(k >> 41) * 0x1p-23f, e1) * ((k & 1) ? -1.f : 1.f);
+    const int e2 = (mix(k + 1) & 1) ? e1 - (int)(mix(k + 2) % 4) : (mode == 0 ? (int)(mix(k + 3) % 277) - 149 : (int)(mix(k + 3) % 41) - 20);
+    const float y = ldexpf(1.0f + (float)(mix(k + 4) >> 41) * 0x1p-23f, e2);
+    bool bad = false;
+    const float h = v1h_fast<true>(x, y, bad);
+    const float ex = v1h(x, y);
+    ++ck;
+    if (!bad) {
+      ++fa;
+      if (__float_as_int(h) != __float_as_int(ex)) ++mi;
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
+}
+
+// every float S in [1, 2]: fast sqrt sequence == __fsqrt_rn
+__global__ void check_sqrt_s_exhaustive(Counts* c) {
+  unsigned long long ck = 0, mi = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= (1u << 23); i += gridDim.x * blockDim.x) {
+    const float S[1] = {__int_as_float(0x3f800000 + i)};
+    float s[1];
+    fast_sqrt_n<1>(S, s);
+    ++ck;
+    if (__float_as_int(s[0]) != __float_as_int(__fsqrt_rn(S[0]))) ++mi;
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
+}
+
+// every float mantissa m in [1,2) against a stride of divisors M in [1,2),
+// with m scaled by 2^-d (d = 0, 1, 12) so that q covers [2^-13, 2):
+// fast division sequence == __fdiv_rn (m <= M only, as in the node)
+__global__ void check_div_s(uint32_t mstride, Counts* c) {
+  unsigned long long ck = 0, mi = 0;
+  const uint32_t nm = 1u << 23;
+  for (uint32_t j = blockIdx.y; j < nm; j += gridDim.y * mstride) {
+    const float M[1] = {__int_as_float(0x3f800000 + j * mstride % nm + (j * 2654435761u >> 9) % mstride)};
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
+      const float mb = __int_as_float(0x3f800000 + i);
+      for (int d = 0; d < 3; ++d) {
+        const float m[1] = {ldexpf(mb, d == 0 ? 0 : (d == 1 ? -1 : -12))};
+        if (m[0] > M[0]) continue;
+        float q[1];
+        fast_div_n<1>(m, M, q);
+        ++ck;
+        if (__float_as_int(q[0]) != __float_as_int(__fdiv_rn(m[0], M[0]))) ++mi;
+      }
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
+}
+
+// fp64 sqrt: S = 1 + k*2^-52 for random k and for k near squares of midpoints
+__global__ void check_sqrt_d(uint64_t seed, uint64_t n, Counts* c) {
+  unsigned long long ck = 0, mi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ i);
+    double Sv;
+    if (i & 1) {
+      Sv = 1.0 + (double)(k >> 12) * 0x1p-52;          // uniform in [1,2)
+    } else {
+      // near a rounding midpoint of sqrt: take t = 1 + j*2^-52 + 2^-53, S = RN(t^2) +- few ulps
+      const double t = 1.0 + (double)((k >> 13) & ((1ull << 51) - 1)) * 0x1p-52 + 0x1p-53;
+      Sv = __dmul_rn(t, t) + (double)((int)(k & 7) - 3) * 0x1p-52;
+      if (Sv < 1.0) Sv = 1.0;
+      if (Sv > 2.0) Sv = 2.0;
+    }
+    const double S[1] = {Sv};
+    double s[1];
+    fast_sqrt_n<1>(S, s);
+    ++ck;
+    if (__double_as_longlong(s[0]) != __double_as_longlong(__dsqrt_rn(Sv))) ++mi;
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
+}
+
+extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long n, int mode,
+                         unsigned long long* out3) {
+  Counts* c;
+  if (cudaMalloc(&c, sizeof(Counts)) != cudaSuccess) return 1;
+  cudaMemset(c, 0, sizeof(Counts));
+  switch (which) {
+    case 0: check_node_d<<<148 * 8, 256>>>(seed, n, mode, c); break;
+    case 1: check_node_s<<<148 * 8, 256>>>(seed, n, mode, c); break;
+    case 2: check_sqrt_s_exhaustive<<<148 * 8, 256>>>(c); break;
+    case 3: check_div_s<<<dim3(64, 2048), 256>>>((uint32_t)n, c); break;
+    case 4: check_sqrt_d<<<148 * 8, 256>>>(seed, n, c); break;
+    default: return 2;
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return 3;
+  Counts h;
+  cudaMemcpy(&h, c, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(c);
+  out3[0] = h.checked; out3[1] = h.fast; out3[2] = h.mism;
+  return 0;
+}

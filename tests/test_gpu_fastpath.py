@@ -1,0 +1,72 @@
+"""GPU check of the fast node sequences against the CUDA
+IEEE-correct intrinsics: wherever a fast node does not flag itself `bad`, its
+result equals the exact-intrinsic node bit for bit; the fp32 square root is
+checked exhaustively on [1, 2], the fp32 division on every dividend mantissa
+against a sample of divisors, fp64 sqrt/node on large random and
+near-midpoint samples."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "csrc", "fastcheck.cu")
+LIB = os.path.join(HERE, "csrc", "libfastcheck.so")
+
+
+@pytest.fixture(scope="module")
+def fc():
+    deps = [SRC, os.path.join(HERE, "..", "paper_2509_06220_b200", "csrc", "nrmf_device.cuh")]
+    if not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in deps):
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                               "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
+                               "-Xcompiler", "-fPIC", "-shared", "-o", LIB, SRC])
+    L = ctypes.CDLL(LIB)
+    L.fastcheck.argtypes = [ctypes.c_int, ctypes.c_ulonglong, ctypes.c_ulonglong, ctypes.c_int,
+                            ctypes.POINTER(ctypes.c_ulonglong)]
+    L.fastcheck.restype = ctypes.c_int
+
+    def run(which, seed=1, n=1 << 26, mode=0):
+        out = (ctypes.c_ulonglong * 3)()
+        assert L.fastcheck(which, seed, n, mode, out) == 0
+        return out[0], out[1], out[2]
+    return run
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fp64_node_fast_equals_exact(fc, mode):
+    checked, fast, mism = fc(0, seed=11 + mode, n=1 << 28, mode=mode)
+    assert checked == 1 << 28 and mism == 0
+    assert fast > (checked // 3 if mode == 0 else checked - checked // 1000)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fp32_node_fast_equals_exact(fc, mode):
+    checked, fast, mism = fc(1, seed=21 + mode, n=1 << 28, mode=mode)
+    assert checked == 1 << 28 and mism == 0
+    assert fast > checked // 3
+
+
+def test_fp32_sqrt_exhaustive_on_1_2(fc):
+    checked, _, mism = fc(2)
+    assert checked == (1 << 23) + 1 and mism == 0
+
+
+def test_fp32_div_all_dividends_sampled_divisors(fc):
+    checked, _, mism = fc(3, n=512)     # every dividend x 2048 divisors x 3 scales
+    assert checked > 4e10 and mism == 0
+
+
+@pytest.mark.slow
+def test_fp32_div_exhaustive(fc):
+    """Every (dividend, divisor) mantissa pair, dividend scaled by 1, 1/2 and
+    2^-12 (q = m/M covers [2^-13, 2)): fast sequence == __fdiv_rn."""
+    checked, _, mism = fc(3, n=1)
+    assert checked > 1.5e14 and mism == 0
+
+
+def test_fp64_sqrt_random_and_near_midpoints(fc):
+    checked, _, mism = fc(4, seed=5, n=1 << 30)
+    assert checked == 1 << 30 and mism == 0
