@@ -31,10 +31,11 @@
  *    Every call is asynchronous and ordered on stream; the library never
  *    synchronizes the device, never allocates device memory and never prints.
  *  - ws is a caller-owned device workspace of at least the size returned by the
- *    matching *_workspace_bytes call.  It must be ZERO-FILLED before its first
- *    use; every call leaves it ready for the next call.  A workspace must not
- *    be shared by calls that may run concurrently (distinct workspaces and
- *    streams make the calls reentrant and thread-safe).
+ *    matching *_workspace_bytes call.  Its contents on entry do not matter
+ *    (the call clears the few bytes of arrival counters it uses, on stream,
+ *    before its kernel).  A workspace must not be shared by calls that may
+ *    run concurrently (distinct workspaces and streams make the calls
+ *    reentrant and thread-safe).
  *  - Status is returned at enqueue time: NRMF_EINVAL for n<0 / null pointers /
  *    bad shapes, NRMF_EALIGN, NRMF_EWORKSPACE, NRMF_ESHARD, NRMF_ECUDA for a
  *    launch error (cudaGetLastError), NRMF_ENCCL for an NCCL error.

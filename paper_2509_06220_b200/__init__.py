@@ -91,8 +91,8 @@ def tree_params(dtype) -> tuple[int, int, int]:
 
 
 # --------------------------------------------------------------- workspaces
-# Zero-filled once, cached per (device, stream, kind); the library leaves a
-# workspace ready for its next call.
+# Cached per (device, stream, kind).  The library clears the arrival counters
+# it uses on every call, so the initial contents do not matter.
 _ws_cache: dict = {}
 
 

@@ -461,6 +461,11 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
   const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
   if (combine && ws_bytes < need) return NRMF_EWORKSPACE;
+  // counters start at zero on every call, whatever the workspace last held
+  // (the last arrivers also leave them zero; this makes reuse of one
+  // workspace across calls of different shapes or functions safe)
+  if (combine && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
+    return NRMF_ECUDA;
   TreeJob<F> job;
   job.x = x;
   job.n_items = n_items;
@@ -572,6 +577,7 @@ static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F*
   F* partials = reinterpret_cast<F*>(base + align_up((size_t)(cols * tpc) * sizeof(F), 256));
   int st = launch_tree<F>(A, cols * tpc, tpc, ld, rows, 1, vals, nullptr, 0, ws, ws_bytes, vec, s);
   if (st != NRMF_OK) return st;
+  if (frob != nullptr && cudaMemsetAsync(ticket, 0, sizeof(unsigned), s) != cudaSuccess) return NRMF_ECUDA;
   const int64_t nblk = (cols + kThreads - 1) / kThreads;
   cols_combine_kernel<F><<<(unsigned)nblk, kThreads, 0, s>>>(vals, cols, tpc, pow2_ceil(tpc), col_norms,
                                                             p2cols, partials, ticket, frob);

@@ -220,6 +220,31 @@ def test_dist_world1(nrmf):
             td.destroy_process_group()
 
 
+def test_workspace_contents_do_not_matter(nrmf):
+    """A workspace full of garbage (0xFF), and one reused across calls of
+    different shapes and functions, gives the same bits."""
+    import ctypes
+    L = nrmf.lib()
+    x = gen.normal(4, 300 * T + 7)
+    xd = dev(x)
+    out = torch.empty((), dtype=torch.float64, device="cuda")
+    nb = L.nrmf_workspace_bytes(x.size, 8)
+    ws = torch.full((nb + 4096,), 0xFF, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    exp = bits(oracle.nrmf(x), np.float64)
+    for _ in range(3):
+        assert L.nrmf_d(x.size, xd.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), s) == 0
+        assert bits(out.cpu().numpy(), np.float64) == exp
+        ws.fill_(0xAB)
+    # interleave column calls of different layouts on one cached workspace
+    for (r, c) in [(9000, 33), (4096, 20000), (9000, 5), (4096, 70000)]:
+        A = gen.colscaled_normal(3, r, c)
+        col, fr = nrmf.cols(dev(A).as_strided((r, c), (1, r)))
+        ecol, efr = oracle.cols(A, r, c, r)
+        assert col.cpu().numpy().tobytes() == ecol.tobytes()
+        assert bits(fr.cpu().numpy(), np.float64) == bits(efr, np.float64)
+
+
 def test_errors_raise(nrmf):
     with pytest.raises(ValueError):
         nrmf.norm(torch.zeros(10, dtype=torch.float16, device="cuda"))
