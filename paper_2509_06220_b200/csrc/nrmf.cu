@@ -138,32 +138,39 @@ __device__ __forceinline__ bool tile_at(const TreeJob<F>& job, int64_t tau, cons
 
 // SMEM-ring loader: the batches of the warp's full tiles, in the order the
 // warp visits them, arrive by TMA bulk copy (cp.async.bulk, mbarrier
-// complete_tx); kBPI batches are consumed per loop iteration.
+// complete_tx); kBPI batches are consumed per loop iteration.  Leaves are read
+// from shared memory per interleaved chunk (get), which keeps only the
+// chunk's leaves in registers.
 template <typename F>
 struct PipeLoader {
   static constexpr int BPI = kBPI;
   static constexpr bool kMaybePadding = false;
   __device__ __forceinline__ bool all_padding(int) const { return false; }
 
-  const unsigned char* ring;  // this warp's kStages x 4 KiB
-  uint32_t ring_s, bar_s;     // shared-window addresses of ring and barriers
+  uint32_t ring_s, bar_s;     // shared-window addresses of this warp's ring and barriers
   uint32_t consumed, issued;  // batches consumed / issued (warp-uniform)
+  uint32_t cur;               // shared address of this thread's 16 B in the current batch 0
   int64_t p_grp;              // producer: warp group of the next tile to load
   int p_k;                    // producer: tile index within that group
   int p_b;                    // producer: batch index within that tile
   const F* p_base;            // producer: base of that tile
-  int64_t W;                  // warp-group stride of this warp
-  int G;                      // tiles per warp group
-  int64_t n_groups;
+  // job geometry (copied: no pointer to the kernel parameter)
+  const F* x;
+  int64_t n_items, tpc, ld, len, W, n_groups;
+  int G;
   uint64_t policy;
-  const TreeJob<F>* job;
 
+  __device__ __forceinline__ bool tile(int64_t tau, const F*& base) const {
+    const int64_t col = tpc == 1 ? tau : tau / tpc;
+    const int64_t tt = tau - col * tpc;
+    base = x + col * ld + tt * (int64_t)kTile;
+    return len - tt * (int64_t)kTile >= kTile;
+  }
   // advance the producer to the next full tile at or after (p_grp, p_k)
   __device__ __forceinline__ void seek_full() {
     while (p_grp < n_groups) {
       const int64_t tau = p_grp * G + p_k;
-      int64_t remv;
-      if (tau < job->n_items && tile_at(*job, tau, p_base, remv)) return;
+      if (tau < n_items && tile(tau, p_base)) return;
       if (++p_k == G) {
         p_k = 0;
         p_grp += W;
@@ -186,31 +193,30 @@ struct PipeLoader {
       seek_full();
     }
   }
-  __device__ __forceinline__ void load(int, F (&u)[kBatch * kBPI][Cfg<F>::V]) {
-    constexpr int V = Cfg<F>::V;
+  __device__ __forceinline__ void begin(int) {
 #pragma unroll
     for (int q = 0; q < kBPI; ++q) {
       const uint32_t c = consumed + q;
-      const uint32_t s = c % kStages;
-      mbar_wait(bar_s + s * 8, (c / kStages) & 1);
-      const unsigned char* buf = ring + s * kBatchBytes + (threadIdx.x & 31) * 16;
-#pragma unroll
-      for (int r = 0; r < kBatch; ++r) {
-        const unsigned char* src = buf + r * (kBatchBytes / kBatch);
-        if constexpr (V == 2) {
-          const double2 d = *reinterpret_cast<const double2*>(src);
-          u[q * kBatch + r][0] = d.x;
-          u[q * kBatch + r][1] = d.y;
-        } else {
-          const float4 d = *reinterpret_cast<const float4*>(src);
-          u[q * kBatch + r][0] = d.x;
-          u[q * kBatch + r][1] = d.y;
-          u[q * kBatch + r][2] = d.z;
-          u[q * kBatch + r][3] = d.w;
-        }
-      }
+      mbar_wait(bar_s + (c % kStages) * 8, (c / kStages) & 1);
     }
-    __syncwarp();  // every lane holds its values: the stages may be refilled
+    cur = ring_s + (consumed % kStages) * kBatchBytes + (threadIdx.x & 31) * 16;
+  }
+  __device__ __forceinline__ F get(int row, int v) const {
+    // row r of the iteration: batch q = r / kBatch (stage consumed+q), row r % kBatch
+    const int q = row / kBatch, rr = row % kBatch;
+    const uint32_t base = (q == 0) ? cur
+        : ring_s + ((consumed + q) % kStages) * kBatchBytes + (threadIdx.x & 31) * 16;
+    const uint32_t addr = base + rr * (kBatchBytes / kBatch) + v * (uint32_t)sizeof(F);
+    F val;
+    if constexpr (sizeof(F) == 8) {
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(val) : "r"(addr) : "memory");
+    } else {
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(val) : "r"(addr) : "memory");
+    }
+    return val;
+  }
+  __device__ __forceinline__ void end(int) {
+    __syncwarp();  // every lane holds its leaves: the stages may be refilled
     consumed += kBPI;
 #pragma unroll
     for (int q = 0; q < kBPI; ++q) issue();
@@ -229,8 +235,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
 
   PipeLoader<F> pl;
   if (kPipe) {
-    pl.ring = smem + w * (kStages * kBatchBytes);
-    pl.ring_s = smem_u32(pl.ring);
+    pl.ring_s = smem_u32(smem + w * (kStages * kBatchBytes));
     pl.bar_s = smem_u32(smem + kWarps * kStages * kBatchBytes) + w * kStages * 8;
     if (lane == 0) {
       for (int st = 0; st < kStages; ++st) mbar_init(pl.bar_s + st * 8, 1);
@@ -244,7 +249,11 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     pl.G = G;
     pl.n_groups = n_groups;
     pl.policy = policy_evict_first();
-    pl.job = &job;
+    pl.x = job.x;
+    pl.n_items = job.n_items;
+    pl.tpc = job.tpc;
+    pl.ld = job.ld;
+    pl.len = job.len;
     pl.seek_full();
     for (int st = 0; st < kStages; ++st) pl.issue();
   }
