@@ -272,6 +272,7 @@ def run_ours(args):
     kern_gbs = cnt * esz / (kern_ms * 1e-3) / 1e9
     clocks = clk.summary()
 
+    f_ghz = (clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) / 1000.0
     line = {
         "metric": METRIC, "value": round(gbs, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
@@ -286,9 +287,13 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(kern_gbs, 2), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(kern_gbs / hbm_peak, 4), "traffic": None,
                      "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs (copy)",
-                     "kernel": "nrmf_tiles_kernel<double|float,VEC=1>",
+                     "kernel": "nrmf_tree_kernel<%s,TMA=1>" % ("double" if esz == 8 else "float"),
                      "algorithmic_bytes_per_launch": cnt * esz},
+        "roofline_compute": compute_roofline(esz, cnt, kern_ms, f_ghz, hbm_peak),
     }
+    tr = load_traffic(esz)
+    if tr is not None:
+        line["roofline"]["traffic"] = tr
     if rank == 0:
         line["result_hex"] = np.asarray(result, dtype=dt).tobytes()[::-1].hex()
 
@@ -366,6 +371,46 @@ def run_ours(args):
     return 0
 
 
+# Compute term of the roofline: per node the
+# stock IEEE sequences execute 21 FP64-pipe instructions (fp64) / 25 issue
+# slots (fp32); these frozen counts are the algorithmic unit.  Peaks from unit
+# counts and the clock sampled during the run: 148 SMs x 64 FP64 lanes/clk;
+# 148 SMs x 4 schedulers x 1 warp-instruction/clk.
+N_SM = 148
+FP64_PER_NODE, ISSUE_PER_NODE_FP32 = 21, 25
+
+
+def compute_roofline(esz, n, ms, f_ghz, hbm_peak):
+    t = ms * 1e-3
+    nodes = max(n - 1, 1)
+    t_hbm = n * esz / (hbm_peak * 1e9)
+    if esz == 8:
+        peak = N_SM * 64 * f_ghz * 1e9                       # FP64 lane-ops/s
+        achieved = nodes * FP64_PER_NODE / t
+        unit, what = "FP64 lane-instr/s", "FP64 pipe (21 instr/node)"
+    else:
+        peak = N_SM * 4 * f_ghz * 1e9                        # warp-instr issued/s
+        achieved = nodes / 32 * ISSUE_PER_NODE_FP32 / t
+        unit, what = "warp-instr/s", "issue (25 slots/node)"
+    t_comp = achieved / peak * t
+    return {"bound": "alu", "pipe": what, "achieved": round(achieved / 1e12, 4), "peak": round(peak / 1e12, 4),
+            "unit": "T " + unit, "frac": round(achieved / peak, 4), "sm_ghz": f_ghz,
+            "t_hbm_ms": round(t_hbm * 1e3, 4), "t_compute_ms": round(t_comp * 1e3, 4),
+            "binding": "hbm" if t_hbm >= t_comp else "alu",
+            "binding_frac": round(max(t_hbm, t_comp) / t, 4)}
+
+
+def load_traffic(esz):
+    """dram bytes read+written per launch of the dominant kernel, from the
+    committed ncu --set full capture of this build (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get("fp64" if esz == 8 else "fp32")
+
+
 def snrmf_point(nrmf, device, stream, args, hbm_peak):
     """The SNRMF half of the metric: fp32 n = 2^30, C2 recipe (s*m*2^e)."""
     import torch
@@ -388,7 +433,9 @@ def snrmf_point(nrmf, device, stream, args, hbm_peak):
     return {"workload": "SNRMF fp32 n=2^30 s*m*2^e, e in [-20,20] (C2 recipe)", "value": round(gbs, 2),
             "unit": "GB/s", "ms_per_step": round(ms, 4),
             "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(gbs / hbm_peak, 4)},
+                         "frac": round(gbs / hbm_peak, 4), "traffic": load_traffic(4)},
+            "roofline_compute": compute_roofline(4, n, ms, (clk.summary().get("sm_mhz") or 1965.0) / 1000.0,
+                                                 hbm_peak),
             "relerr_eps": oracle.relerr(r, ex, np.float32), "ulp": ulp_distance(r, ex, np.float32),
             "clocks": clk.summary()}
 
