@@ -129,31 +129,31 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
 // Tile tau -> (base pointer, full?).  One 64-bit division per tile at most.
 template <typename F>
 __device__ __forceinline__ bool tile_at(const TreeJob<F>& job, int64_t tau, const F*& base, int64_t& remv) {
-  const int64_t col = job.tpc == 1 ? tau : tau / job.tpc;
+  const int64_t col = job.ld == 0 ? 0 : (job.tpc == 1 ? tau : tau / job.tpc);
   const int64_t tt = tau - col * job.tpc;
   base = job.x + col * job.ld + tt * (int64_t)kTile;
   remv = job.len - tt * (int64_t)kTile;
   return remv >= kTile;
 }
 
-// SMEM-ring loader: the batches of the warp's full tiles, in the order the
-// warp visits them, arrive by TMA bulk copy (cp.async.bulk, mbarrier
-// complete_tx); kBPI batches are consumed per loop iteration.  Leaves are read
-// from shared memory per interleaved chunk (get), which keeps only the
-// chunk's leaves in registers.
-template <typename F>
+// SMEM-ring loader: batches of the warp's tile NT-tuples (NT consecutive
+// tiles of a warp group, all full), in the order the warp visits them, arrive
+// by TMA bulk copy (cp.async.bulk, mbarrier complete_tx): for every batch b,
+// one stage per tile of the tuple.  Leaves are read from shared memory per
+// interleaved chunk (get_row), which keeps only the chunk's rows in registers.
+template <typename F, int NT>
 struct PipeLoader {
-  static constexpr int BPI = kBPI;
+  static constexpr int BPI = 1;
   static constexpr bool kMaybePadding = false;
   __device__ __forceinline__ bool all_padding(int) const { return false; }
 
   uint32_t ring_s, bar_s;     // shared-window addresses of this warp's ring and barriers
-  uint32_t consumed, issued;  // batches consumed / issued (warp-uniform)
-  uint32_t cur;               // shared address of this thread's 16 B in the current batch 0
-  int64_t p_grp;              // producer: warp group of the next tile to load
-  int p_k;                    // producer: tile index within that group
-  int p_b;                    // producer: batch index within that tile
-  const F* p_base;            // producer: base of that tile
+  uint32_t consumed, issued;  // stages consumed / issued (warp-uniform)
+  int64_t p_grp;              // producer: warp group of the next tuple to load
+  int p_k;                    // producer: first tile (within the group) of that tuple
+  int p_b;                    // producer: batch index
+  int p_t;                    // producer: tile of the tuple
+  const F* p_base[NT];        // producer: bases of the tuple's tiles
   // job geometry (copied: no pointer to the kernel parameter)
   const F* x;
   int64_t n_items, tpc, ld, len, W, n_groups;
@@ -161,17 +161,27 @@ struct PipeLoader {
   uint64_t policy;
 
   __device__ __forceinline__ bool tile(int64_t tau, const F*& base) const {
-    const int64_t col = tpc == 1 ? tau : tau / tpc;
+    // vector mode (ld == 0): one "column" holding every tile, no division
+    const int64_t col = ld == 0 ? 0 : (tpc == 1 ? tau : tau / tpc);
     const int64_t tt = tau - col * tpc;
     base = x + col * ld + tt * (int64_t)kTile;
     return len - tt * (int64_t)kTile >= kTile;
   }
-  // advance the producer to the next full tile at or after (p_grp, p_k)
-  __device__ __forceinline__ void seek_full() {
+  // is tuple (grp, k) made of NT full tiles with data?
+  __device__ __forceinline__ bool tuple_ok(int64_t grp, int k, const F* (&bases)[NT]) const {
+    bool ok = k + NT <= G;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int64_t tau = grp * G + k + t;
+      ok = ok && tau < n_items && tile(tau, bases[t]);
+    }
+    return ok;
+  }
+  __device__ __forceinline__ void seek() {
     while (p_grp < n_groups) {
-      const int64_t tau = p_grp * G + p_k;
-      if (tau < n_items && tile(tau, p_base)) return;
-      if (++p_k == G) {
+      if (tuple_ok(p_grp, p_k, p_base)) return;
+      p_k += NT;
+      if (p_k >= G) {
         p_k = 0;
         p_grp += W;
       }
@@ -181,49 +191,73 @@ struct PipeLoader {
     if (p_grp >= n_groups) return;
     const uint32_t s = issued % kStages;
     if ((threadIdx.x & 31) == 0)
-      bulk_load(ring_s + s * kBatchBytes, p_base + (int64_t)p_b * kBatch * Cfg<F>::LANES, kBatchBytes,
+      bulk_load(ring_s + s * kBatchBytes, p_base[p_t] + (int64_t)p_b * kBatch * Cfg<F>::LANES, kBatchBytes,
                 bar_s + s * 8, policy);
     ++issued;
-    if (++p_b == Cfg<F>::J / kBatch) {
-      p_b = 0;
-      if (++p_k == G) {
-        p_k = 0;
-        p_grp += W;
+    if (++p_t == NT) {
+      p_t = 0;
+      if (++p_b == Cfg<F>::J / kBatch) {
+        p_b = 0;
+        p_k += NT;
+        if (p_k >= G) {
+          p_k = 0;
+          p_grp += W;
+        }
+        seek();
       }
-      seek_full();
     }
   }
   __device__ __forceinline__ void begin(int) {
 #pragma unroll
-    for (int q = 0; q < kBPI; ++q) {
-      const uint32_t c = consumed + q;
+    for (int t = 0; t < NT; ++t) {
+      const uint32_t c = consumed + t;
       mbar_wait(bar_s + (c % kStages) * 8, (c / kStages) & 1);
     }
-    cur = ring_s + (consumed % kStages) * kBatchBytes + (threadIdx.x & 31) * 16;
   }
-  __device__ __forceinline__ F get(int row, int v) const {
-    // row r of the iteration: batch q = r / kBatch (stage consumed+q), row r % kBatch
-    const int q = row / kBatch, rr = row % kBatch;
-    const uint32_t base = (q == 0) ? cur
-        : ring_s + ((consumed + q) % kStages) * kBatchBytes + (threadIdx.x & 31) * 16;
-    const uint32_t addr = base + rr * (kBatchBytes / kBatch) + v * (uint32_t)sizeof(F);
-    F val;
+  __device__ __forceinline__ void get_row(int t, int row, F (&o)[Cfg<F>::V]) const {
+#ifdef NRMF_FAKE_SMEM  // dev-only timing probe: leaves synthesized in registers (wrong results)
+#pragma unroll
+    for (int v = 0; v < Cfg<F>::V; ++v) o[v] = F(1) + F(row * 7 + v + t) * F(1e-3) + F(consumed & 3);
+    return;
+#endif
+    const uint32_t addr = ring_s + ((consumed + t) % kStages) * kBatchBytes + (threadIdx.x & 31) * 16 +
+                          row * (kBatchBytes / kBatch);
     if constexpr (sizeof(F) == 8) {
-      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(val) : "r"(addr) : "memory");
+      double a0, a1;
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0), "=d"(a1) : "r"(addr) : "memory");
+      o[0] = a0;
+      o[1 % Cfg<F>::V] = a1;
     } else {
-      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(val) : "r"(addr) : "memory");
+      float a0, a1, a2, a3;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3)
+                   : "r"(addr) : "memory");
+      o[0] = a0;
+      o[1 % Cfg<F>::V] = a1;
+      o[2 % Cfg<F>::V] = a2;
+      o[3 % Cfg<F>::V] = a3;
     }
-    return val;
   }
   __device__ __forceinline__ void end(int) {
     __syncwarp();  // every lane holds its leaves: the stages may be refilled
-    consumed += kBPI;
+    consumed += NT;
 #pragma unroll
-    for (int q = 0; q < kBPI; ++q) issue();
+    for (int t = 0; t < NT; ++t) issue();
   }
 };
 
-template <typename F, bool TMA>
+// Value of tile tau when it is not part of a pipelined tuple: a full tile by
+// LDG (fast nodes, exact fallback), a partial one by the exact path, +0 for a
+// padding tile beyond the data.
+template <typename F, bool VEC>
+__device__ __forceinline__ F single_tile(const TreeJob<F>& job, int64_t tau) {
+  if (tau >= job.n_items) return F(0);
+  const F* tb;
+  int64_t remv;
+  if (tile_at(job, tau, tb, remv)) return VEC ? warp_tile<F, kVec>(tb) : warp_tile<F, kScalar>(tb);
+  return warp_tile_exact<F, kPred>(tb, (int)remv);
+}
+
+template <typename F, bool TMA, int NT>
 __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(const TreeJob<F> job) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr bool kPipe = TMA && NRMF_USE_TMA;
@@ -233,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   const int G = 1 << job.g0;
   const int64_t n_groups = (job.n_items + G - 1) >> job.g0;
 
-  PipeLoader<F> pl;
+  PipeLoader<F, NT> pl;
   if (kPipe) {
     pl.ring_s = smem_u32(smem + w * (kStages * kBatchBytes));
     pl.bar_s = smem_u32(smem + kWarps * kStages * kBatchBytes) + w * kStages * 8;
@@ -244,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     __syncwarp();
     pl.consumed = pl.issued = 0;
     pl.p_grp = gw;
-    pl.p_k = pl.p_b = 0;
+    pl.p_k = pl.p_b = pl.p_t = 0;
     pl.W = W;
     pl.G = G;
     pl.n_groups = n_groups;
@@ -254,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     pl.tpc = job.tpc;
     pl.ld = job.ld;
     pl.len = job.len;
-    pl.seek_full();
+    pl.seek();
     for (int st = 0; st < kStages; ++st) pl.issue();
   }
 
@@ -262,32 +296,31 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   unsigned pend_old = 0;
   for (int64_t grp = gw; grp < n_groups; grp += W) {
     F s0[1], s1[1], s2[1], gv[1];
-    for (int k = 0; k < G; ++k) {  // rolled
-      const int64_t tau = grp * G + k;
-      F tv = F(0);  // padding tile beyond the data: its subtree is +0
-      if (tau < job.n_items) {
-        const F* tb;
-        int64_t remv;
-        if (tile_at(job, tau, tb, remv)) {
-          if (kPipe) {
-            NodeFast node;
-            tv = warp_tile_impl<F>(pl, node);
-            if (__any_sync(0xffffffffu, node.bad) || tv != tv) tv = warp_tile_exact<F, kVec>(tb, kTile);
-          } else if (TMA) {
-            tv = warp_tile<F, kVec>(tb);
-          } else {
-            tv = warp_tile<F, kScalar>(tb);
-          }
-        } else {
-          tv = warp_tile_exact<F, kPred>(tb, (int)remv);
-        }
-        if (job.tile_out != nullptr && lane == 0) job.tile_out[tau] = tv;
+    NodeExact ne;
+    for (int k = 0; k < G; k += NT) {  // rolled
+      F tv[NT];
+      const F* bases[NT];
+      if (kPipe && pl.tuple_ok(grp, k, bases)) {
+        NodeFast node;
+        warp_tiles_impl<F, NT>(pl, node, tv);
+        const bool bad = __any_sync(0xffffffffu, node.bad);
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+          if (bad || tv[t] != tv[t]) tv[t] = warp_tile_exact<F, kVec>(bases[t], kTile);
+      } else {
+#pragma unroll
+        for (int t = 0; t < NT; ++t) tv[t] = (k + t < G) ? single_tile<F, TMA>(job, grp * G + k + t) : F(0);
       }
-      gv[0] = tv;
-      NodeExact ne;
-      if (G == 8) counter_merge<F, 1, 8>(k, gv, s0, s1, s2, ne);
-      else if (G == 4) counter_merge<F, 1, 4>(k, gv, s0, s1, s2, ne);
-      else if (G == 2) counter_merge<F, 1, 2>(k, gv, s0, s1, s2, ne);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (k + t >= G) break;
+        const int64_t tau = grp * G + k + t;
+        if (job.tile_out != nullptr && lane == 0 && tau < job.n_items) job.tile_out[tau] = tv[t];
+        gv[0] = tv[t];
+        if (G == 8) counter_merge<F, 1, 8>(k + t, gv, s0, s1, s2, ne);
+        else if (G == 4) counter_merge<F, 1, 4>(k + t, gv, s0, s1, s2, ne);
+        else if (G == 2) counter_merge<F, 1, 2>(k + t, gv, s0, s1, s2, ne);
+      }
     }
     if (!job.combine) continue;
     if (job.nsteps == 0) {  // the warp group is the whole tree
@@ -433,20 +466,25 @@ static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
   return align_up((size_t)pl.n_cnt * 4, 256) + align_up((size_t)pl.n_vals * esz, 256) + 256;
 }
 
+#ifndef NRMF_NT
+#define NRMF_NT 1             // tiles reduced in lockstep per warp when warp groups allow it
+#endif
+
 template <typename F, bool TMA>
 static size_t kernel_smem() {
   return (TMA && NRMF_USE_TMA) ? (size_t)kWarps * kStages * kBatchBytes + (size_t)kWarps * kStages * 8 : 0;
 }
 
-template <typename F, bool TMA>
+template <typename F, bool TMA, int NT>
 static int blocks_per_sm() {
   static int cached = 0;
   if (cached == 0) {
     const size_t sm = kernel_smem<F, TMA>();
     if (sm > 48 * 1024)
-      cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA>, kThreads, sm) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT>, kThreads, sm) !=
+            cudaSuccess ||
         b < 1)
       b = 1;
     cached = b;
@@ -462,10 +500,11 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
                        F* tile_out, F* out, int combine, void* ws, size_t ws_bytes, bool vec,
                        cudaStream_t s) {
   if (n_items == 0) return NRMF_OK;
-  int64_t grid = (int64_t)device_sms() * (vec ? blocks_per_sm<F, true>() : blocks_per_sm<F, false>());
+  int64_t grid = (int64_t)device_sms() * (vec ? blocks_per_sm<F, true, NRMF_NT>() : blocks_per_sm<F, false, 1>());
   if (g_grid_override > 0) grid = g_grid_override;
-  // warp groups of 8 tiles when there is enough work for every warp
-  const int g0_max = n_items >= 8 * grid * kWarps ? 3 : 0;
+  // warp groups of up to 8 tiles while there is enough work for every warp
+  int g0_max = 0;
+  while (g0_max < 3 && n_items >= (int64_t(2) << g0_max) * grid * kWarps) ++g0_max;
   const Plan pl = combine ? make_plan(n_items, p2, g0_max) : make_plan(n_items, 1, 0);
   const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
   const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
@@ -496,10 +535,15 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   }
   const int64_t n_groups = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
   grid = std::min<int64_t>(grid, (n_groups + kWarps - 1) / kWarps);
-  if (vec)
-    nrmf_tree_kernel<F, true><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
-  else
-    nrmf_tree_kernel<F, false><<<(unsigned)grid, kThreads, kernel_smem<F, false>(), s>>>(job);
+  if (vec && pl.g0 >= 1 && NRMF_NT == 2) {
+    blocks_per_sm<F, true, NRMF_NT>();
+    nrmf_tree_kernel<F, true, NRMF_NT><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
+  } else if (vec) {
+    blocks_per_sm<F, true, 1>();
+    nrmf_tree_kernel<F, true, 1><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
+  } else {
+    nrmf_tree_kernel<F, false, 1><<<(unsigned)grid, kThreads, kernel_smem<F, false>(), s>>>(job);
+  }
   return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
 }
 

@@ -59,12 +59,16 @@ __global__ void check_node_s(uint64_t seed, uint64_t n, int mode, Counts* c) {
     const int e2 = (mix(k + 1) & 1) ? e1 - (int)(mix(k + 2) % 4) : (mode == 0 ? (int)(mix(k + 3) % 277) - 149 : (int)(mix(k + 3) % 41) - 20);
     const float y = ldexpf(1.0f + (float)(mix(k + 4) >> 41) * 0x1p-23f, e2);
     bool bad = false;
-    const float h = v1h_fast<true>(x, y, bad);
+    // packed pair: (x, y) and (y, -x) (the node is symmetric and sign-blind)
+    const float xs[2] = {x, y}, ys[2] = {y, -x};
+    float hs[2];
+    v1h_fast_n<true, 2>(xs, ys, hs, bad);
     const float ex = v1h(x, y);
     ++ck;
     if (!bad) {
       ++fa;
-      if (__float_as_int(h) != __float_as_int(ex)) ++mi;
+      if (__float_as_int(hs[0]) != __float_as_int(ex)) ++mi;
+      if (__float_as_int(hs[1]) != __float_as_int(ex)) ++mi;
     }
   }
   atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
@@ -79,6 +83,12 @@ __global__ void check_sqrt_s_exhaustive(Counts* c) {
     fast_sqrt_n<1>(S, s);
     ++ck;
     if (__float_as_int(s[0]) != __float_as_int(__fsqrt_rn(S[0]))) ++mi;
+    // packed (FFMA2/FMUL2) path: pair S with its mirror 3 - S
+    const float S2[2] = {S[0], __int_as_float(0x3f800000 + ((1u << 23) - i))};
+    float s2[2];
+    fast_sqrt_n<2>(S2, s2);
+    if (__float_as_int(s2[0]) != __float_as_int(__fsqrt_rn(S2[0]))) ++mi;
+    if (__float_as_int(s2[1]) != __float_as_int(__fsqrt_rn(S2[1]))) ++mi;
   }
   atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
 }
@@ -93,14 +103,19 @@ __global__ void check_div_s(uint32_t mstride, Counts* c) {
     const float M[1] = {__int_as_float(0x3f800000 + j * mstride % nm + (j * 2654435761u >> 9) % mstride)};
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
       const float mb = __int_as_float(0x3f800000 + i);
-      for (int d = 0; d < 3; ++d) {
-        const float m[1] = {ldexpf(mb, d == 0 ? 0 : (d == 1 ? -1 : -12))};
-        if (m[0] > M[0]) continue;
-        float q[1];
-        fast_div_n<1>(m, M, q);
-        ++ck;
-        if (__float_as_int(q[0]) != __float_as_int(__fdiv_rn(m[0], M[0]))) ++mi;
-      }
+      // packed path (FFMA2): the dividend at scales 1 and 1/2 as one pair,
+      // then at 2^-12 paired with itself; scalar path once per dividend
+      float mm[2] = {mb, ldexpf(mb, -1)}, MM[2] = {M[0], M[0]}, qq[2];
+      if (mm[0] > MM[0]) mm[0] = mm[1];
+      fast_div_n<2>(mm, MM, qq);
+      ck += 2;
+      if (__float_as_int(qq[0]) != __float_as_int(__fdiv_rn(mm[0], MM[0]))) ++mi;
+      if (__float_as_int(qq[1]) != __float_as_int(__fdiv_rn(mm[1], MM[1]))) ++mi;
+      const float m[1] = {ldexpf(mb, -12)};
+      float q[1];
+      fast_div_n<1>(m, M, q);
+      ++ck;
+      if (__float_as_int(q[0]) != __float_as_int(__fdiv_rn(m[0], M[0]))) ++mi;
     }
   }
   atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);

@@ -1,0 +1,28 @@
+"""Dev tool: time nrmf_d / nrmf_s (device-resident input) over sizes."""
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2509_06220_b200 as nrmf  # noqa: E402
+
+
+def t(x, reps=50):
+    out = torch.empty((), dtype=x.dtype, device="cuda")
+    for _ in range(5):
+        nrmf.norm(x, out=out)
+    ts = []
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); nrmf.norm(x, out=out); e1.record(); torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+for dt in (torch.float64, torch.float32):
+    for lg in (12, 16, 18, 20, 22, 24, 26, 28, 30):
+        x = torch.randn(1 << lg, dtype=dt, device="cuda")
+        ms = t(x, 20 if lg >= 28 else 100)
+        print(f"{str(dt):14s} n=2^{lg:2d}: {ms*1e3:9.1f} us  {x.numel()*x.element_size()/ms/1e6:8.1f} GB/s", flush=True)
+        del x
