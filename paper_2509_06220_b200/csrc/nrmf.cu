@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
 
 // Balanced tree over vals[0..P) (entries >= nvals are +0) -> *out.  One CTA.
 template <typename F>
-__global__ void __launch_bounds__(kThreads) bal_kernel(const F* vals, int64_t nvals, int64_t P,
+__global__ void __launch_bounds__(kAuxThreads) bal_kernel(const F* vals, int64_t nvals, int64_t P,
                                                        F* out) {
   const F v = block_bal(vals, nvals, P);
   if (threadIdx.x == 0) *out = v;
@@ -353,11 +353,11 @@ __global__ void __launch_bounds__(kThreads) bal_kernel(const F* vals, int64_t nv
 // values vals[j*tpc ..] padded to p2c; then the frob tree over columns
 // (p2cols = pow2 >= cols) with group partials per CTA and a last-CTA top.
 template <typename F>
-__global__ void __launch_bounds__(kThreads) cols_combine_kernel(
+__global__ void __launch_bounds__(kAuxThreads) cols_combine_kernel(
     const F* vals, int64_t cols, int64_t tpc, int64_t p2c, F* col_norms, int64_t p2cols,
     F* partials, unsigned* ticket, F* frob) {
   __shared__ int s_last;
-  const int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t j = (int64_t)blockIdx.x * kAuxThreads + threadIdx.x;
   F v = F(0);
   if (j < cols) {
     v = seq_bal(vals + j * tpc, tpc, 0, p2c);
@@ -367,14 +367,14 @@ __global__ void __launch_bounds__(kThreads) cols_combine_kernel(
   // block level: first min(8, lg p2cols) levels of the frob tree
   const int lg = ilog2_64(p2cols);
   const int bl = lg < 8 ? lg : 8;
-  __shared__ F sh[kWarps];
+  __shared__ F sh[kAuxWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wl = bl < 5 ? bl : 5;
   for (int l = 0; l < wl; ++l) v = v1h(v, __shfl_xor_sync(0xffffffffu, v, 1 << l));
   if (bl > 5) {
     if (lane == 0) sh[w] = v;
     __syncthreads();
-    v = lane < kWarps ? sh[lane] : F(0);
+    v = lane < kAuxWarps ? sh[lane] : F(0);
     for (int l = 0; l < bl - 5; ++l) v = v1h(v, __shfl_xor_sync(0xffffffffu, v, 1 << l));
   }
   const int64_t pb = p2cols >> bl;  // values left after the block levels
@@ -565,7 +565,7 @@ template int tree_eval<float>(int64_t, const float*, int64_t, float*, void*, siz
 
 template <typename F>
 int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s) {
-  bal_kernel<F><<<1, kThreads, 0, s>>>(vals, nvals, P, out);
+  bal_kernel<F><<<1, kAuxThreads, 0, s>>>(vals, nvals, P, out);
   return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
 }
 template int bal_eval<double>(const double*, int64_t, int64_t, double*, cudaStream_t);
@@ -594,7 +594,7 @@ static size_t cols_ws_bytes(int64_t rows, int64_t cols, size_t esz) {
   const int64_t tpc = std::max<int64_t>((rows + kTile - 1) / kTile, 1);
   const int64_t p2cols = pow2_ceil(std::max<int64_t>(cols, 1));
   if (tpc == 1) return tree_ws_bytes(std::max<int64_t>(cols, 1), p2cols, esz);
-  const int64_t nblk = (cols + kThreads - 1) / kThreads;
+  const int64_t nblk = (cols + kAuxThreads - 1) / kAuxThreads;
   return 256 + align_up((size_t)(cols * tpc) * esz, 256) + align_up((size_t)std::max<int64_t>(nblk, 1) * esz, 256);
 }
 
@@ -631,8 +631,8 @@ static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F*
   int st = launch_tree<F>(A, cols * tpc, tpc, ld, rows, 1, vals, nullptr, 0, ws, ws_bytes, vec, s);
   if (st != NRMF_OK) return st;
   if (frob != nullptr && cudaMemsetAsync(ticket, 0, sizeof(unsigned), s) != cudaSuccess) return NRMF_ECUDA;
-  const int64_t nblk = (cols + kThreads - 1) / kThreads;
-  cols_combine_kernel<F><<<(unsigned)nblk, kThreads, 0, s>>>(vals, cols, tpc, pow2_ceil(tpc), col_norms,
+  const int64_t nblk = (cols + kAuxThreads - 1) / kAuxThreads;
+  cols_combine_kernel<F><<<(unsigned)nblk, kAuxThreads, 0, s>>>(vals, cols, tpc, pow2_ceil(tpc), col_norms,
                                                             p2cols, partials, ticket, frob);
   return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
 }
