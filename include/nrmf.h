@@ -66,6 +66,18 @@ typedef enum {
     NRMF_ENCCL = 6        /* NCCL error, or NCCL could not be loaded                   */
 } nrmf_status;
 
+/* Flags of the *_ex_* calls.
+ * NRMF_TOP_CR: every node ABOVE the tile level (warp groups, grid steps,
+ *   column trees, the Frobenius tree over columns, host chunks, ranks) uses
+ *   the correctly rounded hypot cr_hypot(a,b) = RN(sqrt(a^2+b^2)) instead of
+ *   v1_hypot -- the paper's recommended final reduction "Z with A"
+ *   (A_x = R with cr_hypot).  The tiles keep v1_hypot.
+ *   Relative error bound: ((1+eps'+)^lg T * (1+eps)^lg(P2) - 1)/eps, e.g.
+ *   36 + 18 = 54 eps at n = 2^30 fp64 (< 64: the 64-eps target becomes a
+ *   theorem).  cr_hypot follows IEEE 754 hypot for specials
+ *   (+inf if either operand is infinite, else NaN if either is NaN). */
+#define NRMF_TOP_CR 1
+
 /* Human-readable name of a status code (static string). */
 const char *nrmf_status_str(int status);
 
@@ -81,6 +93,10 @@ int nrmf_tree_params(int elem_bytes, int *lanes, int *J, int *tile);
 size_t nrmf_workspace_bytes(int64_t n, int elem_bytes);
 int nrmf_d(int64_t n, const double *x, double *out, void *ws, size_t ws_bytes, void *stream);
 int nrmf_s(int64_t n, const float *x, float *out, void *ws, size_t ws_bytes, void *stream);
+
+/* The same with flags (NRMF_TOP_CR or 0); flags 0 is bitwise nrmf_[ds]. */
+int nrmf_ex_d(int64_t n, const double *x, double *out, int flags, void *ws, size_t ws_bytes, void *stream);
+int nrmf_ex_s(int64_t n, const float *x, float *out, int flags, void *ws, size_t ws_bytes, void *stream);
 
 /* Complex view (e:F: the real and imaginary parts are just more
  * elements): ||z||_F of count interleaved (re,im) pairs; bitwise identical to
@@ -100,6 +116,10 @@ int nrmf_cols_d(int64_t rows, int64_t cols, int64_t ld, const double *A, double 
                 double *frob, void *ws, size_t ws_bytes, void *stream);
 int nrmf_cols_s(int64_t rows, int64_t cols, int64_t ld, const float *A, float *col_norms,
                 float *frob, void *ws, size_t ws_bytes, void *stream);
+int nrmf_cols_ex_d(int64_t rows, int64_t cols, int64_t ld, const double *A, double *col_norms,
+                   double *frob, int flags, void *ws, size_t ws_bytes, void *stream);
+int nrmf_cols_ex_s(int64_t rows, int64_t cols, int64_t ld, const float *A, float *col_norms,
+                   float *frob, int flags, void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* Host-resident input (pinned memory for overlap): streams host_x through a  */
@@ -113,6 +133,10 @@ int nrmf_host_d(int64_t n, const double *host_x, double *host_out, void *ws, siz
                 void *stream);
 int nrmf_host_s(int64_t n, const float *host_x, float *host_out, void *ws, size_t ws_bytes,
                 void *stream);
+int nrmf_host_ex_d(int64_t n, const double *host_x, double *host_out, int flags, void *ws,
+                   size_t ws_bytes, void *stream);
+int nrmf_host_ex_s(int64_t n, const float *host_x, float *host_out, int flags, void *ws,
+                   size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* One array sharded contiguously over the `world` ranks of an NCCL          */
@@ -133,6 +157,10 @@ int nrmf_dist_d(int64_t n_global, int64_t offset, int64_t count, const double *x
                 double *out, void *ws, size_t ws_bytes, void *nccl_comm, void *stream);
 int nrmf_dist_s(int64_t n_global, int64_t offset, int64_t count, const float *x_local,
                 float *out, void *ws, size_t ws_bytes, void *nccl_comm, void *stream);
+int nrmf_dist_ex_d(int64_t n_global, int64_t offset, int64_t count, const double *x_local,
+                   double *out, int flags, void *ws, size_t ws_bytes, void *nccl_comm, void *stream);
+int nrmf_dist_ex_s(int64_t n_global, int64_t offset, int64_t count, const float *x_local,
+                   float *out, int flags, void *ws, size_t ws_bytes, void *nccl_comm, void *stream);
 
 /* NCCL bootstrap helpers (libnccl.so.2 is loaded at first use; the process's
  * already-loaded NCCL, e.g. torch's, is reused).  id is 128 bytes: create it

@@ -63,13 +63,20 @@ def lib():
         L.oracle_v1_hypot_array_s.argtypes = [i64, vp, vp, vp]; L.oracle_v1_hypot_array_s.restype = None
         L.oracle_R_H_d.argtypes = [i64, vp]; L.oracle_R_H_d.restype = d
         L.oracle_R_H_s.argtypes = [i64, vp]; L.oracle_R_H_s.restype = f
-        L.oracle_nrmf_tree_d.argtypes = [vp, i64, i64, i64, i64, ip]; L.oracle_nrmf_tree_d.restype = d
-        L.oracle_nrmf_tree_s.argtypes = [vp, i64, i64, i64, i64, ip]; L.oracle_nrmf_tree_s.restype = f
+        ci = ctypes.c_int
+        L.oracle_nrmf_tree_d.argtypes = [vp, i64, i64, i64, i64, ci, ip]; L.oracle_nrmf_tree_d.restype = d
+        L.oracle_nrmf_tree_s.argtypes = [vp, i64, i64, i64, i64, ci, ip]; L.oracle_nrmf_tree_s.restype = f
+        L.oracle_cr_hypot_d.argtypes = [d, d]; L.oracle_cr_hypot_d.restype = d
+        L.oracle_cr_hypot_s.argtypes = [f, f]; L.oracle_cr_hypot_s.restype = f
+        L.oracle_cr_hypot_array_d.argtypes = [i64, vp, vp, vp]; L.oracle_cr_hypot_array_d.restype = None
+        L.oracle_cr_hypot_array_s.argtypes = [i64, vp, vp, vp]; L.oracle_cr_hypot_array_s.restype = None
+        L.oracle_R_A_d.argtypes = [i64, vp]; L.oracle_R_A_d.restype = d
+        L.oracle_R_A_s.argtypes = [i64, vp]; L.oracle_R_A_s.restype = f
         L.oracle_tiles_d.argtypes = [vp, i64, i64, i64, i64, i64, vp]; L.oracle_tiles_d.restype = ctypes.c_int
         L.oracle_tiles_s.argtypes = [vp, i64, i64, i64, i64, i64, vp]; L.oracle_tiles_s.restype = ctypes.c_int
-        L.oracle_nrmf_cols_d.argtypes = [i64, i64, i64, vp, i64, i64, vp, vp]
+        L.oracle_nrmf_cols_d.argtypes = [i64, i64, i64, vp, i64, i64, ctypes.c_int, vp, vp]
         L.oracle_nrmf_cols_d.restype = ctypes.c_int
-        L.oracle_nrmf_cols_s.argtypes = [i64, i64, i64, vp, i64, i64, vp, vp]
+        L.oracle_nrmf_cols_s.argtypes = [i64, i64, i64, vp, i64, i64, ctypes.c_int, vp, vp]
         L.oracle_nrmf_cols_s.restype = ctypes.c_int
         for sfx in ("d", "s"):
             getattr(L, "exact_acc_" + sfx).argtypes = [vp, i64, vp, ip]
@@ -114,6 +121,31 @@ def v1_hypot_array(x, y):
     return out
 
 
+def cr_hypot(x, y, dtype=np.float64):
+    """Correctly rounded hypot: RN(sqrt(x^2+y^2)) exactly (IEEE specials)."""
+    if np.dtype(dtype) == np.float64:
+        return np.float64(lib().oracle_cr_hypot_d(float(x), float(y)))
+    return np.float32(lib().oracle_cr_hypot_s(float(np.float32(x)), float(np.float32(y))))
+
+
+def cr_hypot_array(x, y):
+    """cr_hypot applied elementwise."""
+    x = _arr(x)
+    y = _arr(y, x.dtype)
+    out = np.empty_like(x)
+    f = lib().oracle_cr_hypot_array_d if _is64(x) else lib().oracle_cr_hypot_array_s
+    f(x.size, x.ctypes.data, y.ctypes.data, out.ctypes.data)
+    return out
+
+
+def R_A(x):
+    """Listing 1 with cr_hypot (the A algorithm)."""
+    x = _arr(x)
+    assert x.size >= 1
+    f = lib().oracle_R_A_d if _is64(x) else lib().oracle_R_A_s
+    return x.dtype.type(f(x.size, x.ctypes.data))
+
+
 def R_H(x):
     """Listing 1 (scalar recursive, ceil split) with v1_hypot; n >= 1."""
     x = _arr(x)
@@ -122,10 +154,11 @@ def R_H(x):
     return x.dtype.type(f(x.size, x.ctypes.data))
 
 
-def nrmf(x, lanes: int | None = None, J: int | None = None, p2_min: int = 1):
+def nrmf(x, lanes: int | None = None, J: int | None = None, p2_min: int = 1, top: str = "v1"):
     """The tile-lane tree.  lanes/J default to the production tree of x's dtype.
     lanes=1, J>=n (power of two) is Listing 1; lanes=8 is Z_D with an
-    R-with-v1_hypot final reduction."""
+    R-with-v1_hypot final reduction.  top="cr": the levels
+    above the tiles use cr_hypot (the A-style final reduction)."""
     x = _arr(x)
     dl, dj = TREE[x.dtype]
     lanes = dl if lanes is None else lanes
@@ -133,7 +166,7 @@ def nrmf(x, lanes: int | None = None, J: int | None = None, p2_min: int = 1):
     assert lanes & (lanes - 1) == 0 and J & (J - 1) == 0
     ok = ctypes.c_int(1)
     f = lib().oracle_nrmf_tree_d if _is64(x) else lib().oracle_nrmf_tree_s
-    r = f(x.ctypes.data, x.size, lanes, J, p2_min, ctypes.byref(ok))
+    r = f(x.ctypes.data, x.size, lanes, J, p2_min, 1 if top == "cr" else 0, ctypes.byref(ok))
     if not ok.value:
         raise MemoryError("oracle: allocation failed")
     return x.dtype.type(r)
@@ -155,7 +188,7 @@ def tiles(x, tau0: int = 0, count: int | None = None, lanes=None, J=None):
     return out
 
 
-def cols(A, r: int, c: int, ld: int, lanes=None, J=None):
+def cols(A, r: int, c: int, ld: int, lanes=None, J=None, top: str = "v1"):
     """Column norms of the column-major r x c matrix stored in flat A (leading
     dimension ld), and the Frobenius norm (R_H over the padded column norms)."""
     A = _arr(A)
@@ -165,13 +198,14 @@ def cols(A, r: int, c: int, ld: int, lanes=None, J=None):
     col = np.empty(c, dtype=A.dtype)
     frob = np.zeros(1, dtype=A.dtype)
     f = lib().oracle_nrmf_cols_d if _is64(A) else lib().oracle_nrmf_cols_s
-    if not f(r, c, ld, A.ctypes.data, lanes, J, col.ctypes.data, frob.ctypes.data):
+    if not f(r, c, ld, A.ctypes.data, lanes, J, 1 if top == "cr" else 0, col.ctypes.data, frob.ctypes.data):
         raise MemoryError("oracle: allocation failed")
     return col, A.dtype.type(frob[0])
 
 
-def combine(values):
-    """R_H over the list padded with +0 to a power of two (the rank tree)."""
+def combine(values, top: str = "v1"):
+    """R_H (or R_A for top="cr") over the list padded with +0 to a power of two
+    (the rank tree)."""
     v = _arr(values)
     if v.size == 0:
         return v.dtype.type(0)
@@ -180,7 +214,7 @@ def combine(values):
         p <<= 1
     pad = np.zeros(p, dtype=v.dtype)
     pad[: v.size] = v
-    return R_H(pad)
+    return R_A(pad) if top == "cr" else R_H(pad)
 
 
 def shard_ranges(n: int, G: int, T: int = 4096):
@@ -206,7 +240,7 @@ def shard_ranges(n: int, G: int, T: int = 4096):
     return out
 
 
-def shard_norms(x, G: int):
+def shard_norms(x, G: int, top: str = "v1"):
     """Value of each rank's aligned subtree (oracle), in rank order."""
     x = _arr(x)
     dl, dj = TREE[x.dtype]
@@ -215,14 +249,14 @@ def shard_norms(x, G: int):
         if p2l == 0:
             res.append(None)
         else:
-            res.append(nrmf(x[a:a + cnt], p2_min=p2l))
+            res.append(nrmf(x[a:a + cnt], p2_min=p2l, top=top))
     return res
 
 
-def combine_ranks(values):
-    """Rank tree: R_H over the values of ranks that own part of the tree."""
+def combine_ranks(values, top: str = "v1"):
+    """Rank tree: R_H (R_A) over the values of ranks that own part of the tree."""
     vals = [v for v in values if v is not None]
-    return combine(np.array(vals, dtype=type(vals[0])))
+    return combine(np.array(vals, dtype=type(vals[0])), top=top)
 
 
 def exact(x, threads: int | None = None):

@@ -107,6 +107,64 @@ float oracle_R_H_s(int64_t n, const float *x)
 }
 
 /* ------------------------------------------------------------------------- */
+/* 2b. cr_hypot ("correctly rounded hypotenuse functions") and the   */
+/*     A variant of Listing 1 (A_x = R with cr_hypot).  The plain    */
+/*     definition written out: RN(sqrt(x^2 + y^2)) computed exactly by the     */
+/*     exact reference of section 5; IEEE 754 hypot specials: +inf if either   */
+/*     operand is infinite (even with a NaN), else NaN if either is NaN.        */
+/* ------------------------------------------------------------------------- */
+double exact_nrm_d(const double *x, int64_t n);
+float exact_nrm_s(const float *x, int64_t n);
+
+double oracle_cr_hypot_d(double x, double y)
+{
+    if (isinf(x) || isinf(y)) return INFINITY;
+    if (isnan(x) || isnan(y)) return NAN;
+    const double v[2] = {x, y};
+    return exact_nrm_d(v, 2);
+}
+
+float oracle_cr_hypot_s(float x, float y)
+{
+    if (isinf(x) || isinf(y)) return INFINITY;
+    if (isnan(x) || isnan(y)) return NAN;
+    const float v[2] = {x, y};
+    return exact_nrm_s(v, 2);
+}
+
+void oracle_cr_hypot_array_d(int64_t n, const double *x, const double *y, double *out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_cr_hypot_d(x[i], y[i]);
+}
+
+void oracle_cr_hypot_array_s(int64_t n, const float *x, const float *y, float *out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_cr_hypot_s(x[i], y[i]);
+}
+
+double oracle_R_A_d(int64_t n, const double *x)
+{
+    if (n == 1) return fabs(*x);
+    if (n == 2) return oracle_cr_hypot_d(x[0], x[1]);
+    const int64_t p = ((n >> 1) + (n & 1));
+    const int64_t q = (n - p);
+    const double fp = oracle_R_A_d(p, x);
+    const double fq = oracle_R_A_d(q, x + p);
+    return oracle_cr_hypot_d(fp, fq);
+}
+
+float oracle_R_A_s(int64_t n, const float *x)
+{
+    if (n == 1) return fabsf(*x);
+    if (n == 2) return oracle_cr_hypot_s(x[0], x[1]);
+    const int64_t p = ((n >> 1) + (n & 1));
+    const int64_t q = (n - p);
+    const float fp = oracle_R_A_s(p, x);
+    const float fq = oracle_R_A_s(q, x + p);
+    return oracle_cr_hypot_s(fp, fq);
+}
+
+/* ------------------------------------------------------------------------- */
 /* 3. The tile-lane tree (DESIGN.md §3 / SURVEY Appendix A).                  */
 /*                                                                           */
 /*   lanes = number of lanes p (fp64 production: 64, fp32: 128)               */
@@ -162,7 +220,7 @@ float oracle_tile_s(const float *x, int64_t n, int64_t lanes, int64_t J,
 /* same tree as an aligned subtree of a bigger one (used by the shard tests). */
 /* Returns -1 status through *ok = 0 on allocation failure.                   */
 double oracle_nrmf_tree_d(const double *x, int64_t n, int64_t lanes, int64_t J,
-                          int64_t p2_min, int *ok)
+                          int64_t p2_min, int top_cr, int *ok)
 {
     *ok = 1;
     if (n == 0 && p2_min <= 1) return 0.0;               /* n = 0 -> +0 (R5) */
@@ -174,13 +232,15 @@ double oracle_nrmf_tree_d(const double *x, int64_t n, int64_t lanes, int64_t J,
     if (!tiles || !scratch) { free(tiles); free(scratch); *ok = 0; return 0.0; }
     for (int64_t tau = 0; tau < NT; ++tau)
         tiles[tau] = oracle_tile_d(x, n, lanes, J, tau, scratch);
-    const double r = oracle_R_H_d(P2, tiles);
+    /* top levels (above the tiles): v1_hypot, or cr_hypot for the A-style
+       final reduction (R1 / SURVEY f1) */
+    const double r = top_cr ? oracle_R_A_d(P2, tiles) : oracle_R_H_d(P2, tiles);
     free(tiles); free(scratch);
     return r;
 }
 
 float oracle_nrmf_tree_s(const float *x, int64_t n, int64_t lanes, int64_t J,
-                         int64_t p2_min, int *ok)
+                         int64_t p2_min, int top_cr, int *ok)
 {
     *ok = 1;
     if (n == 0 && p2_min <= 1) return 0.0f;
@@ -192,7 +252,7 @@ float oracle_nrmf_tree_s(const float *x, int64_t n, int64_t lanes, int64_t J,
     if (!tiles || !scratch) { free(tiles); free(scratch); *ok = 0; return 0.0f; }
     for (int64_t tau = 0; tau < NT; ++tau)
         tiles[tau] = oracle_tile_s(x, n, lanes, J, tau, scratch);
-    const float r = oracle_R_H_s(P2, tiles);
+    const float r = top_cr ? oracle_R_A_s(P2, tiles) : oracle_R_H_s(P2, tiles);
     free(tiles); free(scratch);
     return r;
 }
@@ -226,11 +286,11 @@ int oracle_tiles_s(const float *x, int64_t n, int64_t lanes, int64_t J,
 /*    to a power of two.                                                      */
 /* ------------------------------------------------------------------------- */
 int oracle_nrmf_cols_d(int64_t r, int64_t c, int64_t ld, const double *A,
-                       int64_t lanes, int64_t J, double *col_norms, double *frob)
+                       int64_t lanes, int64_t J, int top_cr, double *col_norms, double *frob)
 {
     int ok = 1;
     for (int64_t j = 0; j < c; ++j) {
-        col_norms[j] = oracle_nrmf_tree_d(A + j * ld, r, lanes, J, 1, &ok);
+        col_norms[j] = oracle_nrmf_tree_d(A + j * ld, r, lanes, J, 1, top_cr, &ok);
         if (!ok) return 0;
     }
     if (frob) {
@@ -239,18 +299,18 @@ int oracle_nrmf_cols_d(int64_t r, int64_t c, int64_t ld, const double *A,
         double *v = (double *)calloc((size_t)P, sizeof(double));
         if (!v) return 0;
         memcpy(v, col_norms, (size_t)c * sizeof(double));
-        *frob = oracle_R_H_d(P, v);
+        *frob = top_cr ? oracle_R_A_d(P, v) : oracle_R_H_d(P, v);
         free(v);
     }
     return 1;
 }
 
 int oracle_nrmf_cols_s(int64_t r, int64_t c, int64_t ld, const float *A,
-                       int64_t lanes, int64_t J, float *col_norms, float *frob)
+                       int64_t lanes, int64_t J, int top_cr, float *col_norms, float *frob)
 {
     int ok = 1;
     for (int64_t j = 0; j < c; ++j) {
-        col_norms[j] = oracle_nrmf_tree_s(A + j * ld, r, lanes, J, 1, &ok);
+        col_norms[j] = oracle_nrmf_tree_s(A + j * ld, r, lanes, J, 1, top_cr, &ok);
         if (!ok) return 0;
     }
     if (frob) {
@@ -259,7 +319,7 @@ int oracle_nrmf_cols_s(int64_t r, int64_t c, int64_t ld, const float *A,
         float *v = (float *)calloc((size_t)P, sizeof(float));
         if (!v) return 0;
         memcpy(v, col_norms, (size_t)c * sizeof(float));
-        *frob = oracle_R_H_s(P, v);
+        *frob = top_cr ? oracle_R_A_s(P, v) : oracle_R_H_s(P, v);
         free(v);
     }
     return 1;

@@ -27,6 +27,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libnrmf.so")
 
 NRMF_OK = 0
+NRMF_TOP_CR = 1   # include/nrmf.h: cr_hypot above the tile level (A-style final reduction)
 _lib = None
 _lock = threading.Lock()
 
@@ -51,6 +52,15 @@ def _load():
         L.nrmf_dist_workspace_bytes.argtypes = [i64, i32, i32]; L.nrmf_dist_workspace_bytes.restype = sz
         for f in ("nrmf_d", "nrmf_s", "nrmf_z_d", "nrmf_z_s", "nrmf_host_d", "nrmf_host_s"):
             getattr(L, f).argtypes = [i64, vp, vp, vp, sz, vp]
+            getattr(L, f).restype = i32
+        for f in ("nrmf_ex_d", "nrmf_ex_s", "nrmf_host_ex_d", "nrmf_host_ex_s"):
+            getattr(L, f).argtypes = [i64, vp, vp, i32, vp, sz, vp]
+            getattr(L, f).restype = i32
+        for f in ("nrmf_cols_ex_d", "nrmf_cols_ex_s"):
+            getattr(L, f).argtypes = [i64, i64, i64, vp, vp, vp, i32, vp, sz, vp]
+            getattr(L, f).restype = i32
+        for f in ("nrmf_dist_ex_d", "nrmf_dist_ex_s"):
+            getattr(L, f).argtypes = [i64, i64, i64, vp, vp, i32, vp, sz, vp, vp]
             getattr(L, f).restype = i32
         for f in ("nrmf_cols_d", "nrmf_cols_s"):
             getattr(L, f).argtypes = [i64, i64, i64, vp, vp, vp, vp, sz, vp]
@@ -109,6 +119,14 @@ def clear_workspaces():
     _ws_cache.clear()
 
 
+def _flags(top: str) -> int:
+    if top == "v1":
+        return 0
+    if top == "cr":
+        return NRMF_TOP_CR
+    raise ValueError(f"nrmf: top must be 'v1' or 'cr', got {top!r}")
+
+
 def _elem(dtype) -> tuple[int, str]:
     if dtype == torch.float64:
         return 8, "d"
@@ -118,12 +136,14 @@ def _elem(dtype) -> tuple[int, str]:
 
 
 # --------------------------------------------------------------- public API
-def norm(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+def norm(x: torch.Tensor, out: torch.Tensor | None = None, top: str = "v1") -> torch.Tensor:
     """||x||_F by the xNRMF tree (bitwise reproducible).
 
     CUDA tensor: enqueued on the current stream, returns a 0-d CUDA tensor.
     CPU tensor (pin it for copy/compute overlap): streamed through the current
-    CUDA device; synchronizes and returns a 0-d CPU tensor."""
+    CUDA device; synchronizes and returns a 0-d CPU tensor.
+    top="cr": correctly rounded hypot above the tile level (NRMF_TOP_CR)."""
+    fl = _flags(top)
     if not x.is_contiguous():
         raise ValueError("nrmf.norm: tensor must be contiguous")
     esz, c = _elem(x.dtype)
@@ -136,8 +156,8 @@ def norm(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
             if out is None:
                 out = torch.empty((), dtype=x.dtype, device=dev)
             ws = _workspace(L.nrmf_workspace_bytes(n, esz), dev, s, "vec")
-            f = L.nrmf_d if c == "d" else L.nrmf_s
-            _check(f(n, x.data_ptr() if n else None, out.data_ptr(), ws.data_ptr(), ws.numel(),
+            f = L.nrmf_ex_d if c == "d" else L.nrmf_ex_s
+            _check(f(n, x.data_ptr() if n else None, out.data_ptr(), fl, ws.data_ptr(), ws.numel(),
                      s.cuda_stream), "nrmf.norm")
         return out
     # host input
@@ -146,8 +166,8 @@ def norm(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     if out is None:
         out = torch.empty((), dtype=x.dtype).pin_memory()
     ws = _workspace(L.nrmf_host_workspace_bytes(n, esz), dev, s, "host")
-    f = L.nrmf_host_d if c == "d" else L.nrmf_host_s
-    _check(f(n, x.data_ptr() if n else None, out.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream),
+    f = L.nrmf_host_ex_d if c == "d" else L.nrmf_host_ex_s
+    _check(f(n, x.data_ptr() if n else None, out.data_ptr(), fl, ws.data_ptr(), ws.numel(), s.cuda_stream),
            "nrmf.norm(host)")
     s.synchronize()
     return out
@@ -176,9 +196,10 @@ def norm_complex(z: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def cols(A: torch.Tensor, frob: bool = True):
+def cols(A: torch.Tensor, frob: bool = True, top: str = "v1"):
     """Column norms and Frobenius norm of a column-major CUDA matrix
     (A.stride(0) == 1, ld = A.stride(1)); e.g. ``B.t()`` of a row-major B."""
+    fl = _flags(top)
     if A.dim() != 2:
         raise ValueError("nrmf.cols: 2-D tensor expected")
     r, c = A.shape
@@ -197,9 +218,9 @@ def cols(A: torch.Tensor, frob: bool = True):
         col = torch.empty(c, dtype=A.dtype, device=dev)
         fr = torch.empty((), dtype=A.dtype, device=dev) if frob else None
         ws = _workspace(L.nrmf_cols_workspace_bytes(r, c, esz), dev, s, "cols")
-        f = L.nrmf_cols_d if ch == "d" else L.nrmf_cols_s
+        f = L.nrmf_cols_ex_d if ch == "d" else L.nrmf_cols_ex_s
         _check(f(r, c, ld, A.data_ptr() if A.numel() else None, col.data_ptr() if c else None,
-                 fr.data_ptr() if fr is not None else None, ws.data_ptr(), ws.numel(), s.cuda_stream),
+                 fr.data_ptr() if fr is not None else None, fl, ws.data_ptr(), ws.numel(), s.cuda_stream),
                "nrmf.cols")
     return (col, fr) if frob else col
 
@@ -252,13 +273,14 @@ def comm_for(group=None) -> Comm:
 
 
 def dist(x_local: torch.Tensor, n_global: int, group=None, comm: Comm | None = None,
-         out: torch.Tensor | None = None) -> torch.Tensor:
+         out: torch.Tensor | None = None, top: str = "v1") -> torch.Tensor:
     """||x||_F of an array of n_global elements sharded canonically over the
     ranks of `group` (x_local = this rank's shard, see shard()).  Collective;
     returns the same 0-d CUDA tensor bits on every rank."""
     if not x_local.is_cuda or not x_local.is_contiguous():
         raise ValueError("nrmf.dist: contiguous CUDA tensor expected")
     esz, c = _elem(x_local.dtype)
+    fl = _flags(top)
     comm = comm or comm_for(group)
     off, cnt = shard(n_global, comm.world, comm.rank)
     if x_local.numel() != cnt:
@@ -270,8 +292,8 @@ def dist(x_local: torch.Tensor, n_global: int, group=None, comm: Comm | None = N
         if out is None:
             out = torch.empty((), dtype=x_local.dtype, device=dev)
         ws = _workspace(L.nrmf_dist_workspace_bytes(n_global, comm.world, esz), dev, s, "dist")
-        f = L.nrmf_dist_d if c == "d" else L.nrmf_dist_s
-        _check(f(n_global, off, cnt, x_local.data_ptr() if cnt else None, out.data_ptr(), ws.data_ptr(),
+        f = L.nrmf_dist_ex_d if c == "d" else L.nrmf_dist_ex_s
+        _check(f(n_global, off, cnt, x_local.data_ptr() if cnt else None, out.data_ptr(), fl, ws.data_ptr(),
                  ws.numel(), comm.handle, s.cuda_stream), "nrmf.dist")
     return out
 

@@ -8,7 +8,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libnrmf.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("nrmf.cu", "nrmf_dist.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("nrmf_device.cuh", "nrmf_internal.h")] + [
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("nrmf_device.cuh", "nrmf_internal.h",
+                                                           "nrmf_crhypot.cuh")] + [
     os.path.join(ROOT, "include", "nrmf.h")]
 
 NVCC_FLAGS = [

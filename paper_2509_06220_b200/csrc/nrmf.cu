@@ -59,6 +59,7 @@ struct TreeJob {
   unsigned* cnt;       // workspace: arrival counters of every step (zero between calls)
   F* out;              // root of the tree; unused if !combine
   int combine;         // 0: only write tile values
+  int top_cr;          // levels above the tiles use cr_hypot (NRMF_TOP_CR)
   int g0;              // tile-tree levels combined inside a warp group (<= 3)
   int nsteps;          // combine steps above the warp groups
   int lg_fan[kMaxSteps];
@@ -70,7 +71,7 @@ struct TreeJob {
 // One warp evaluates the balanced tree over 2^f (<= 64) consecutive values
 // vals[base ..] (entries >= nvals are +0).  All lanes return the value.
 template <typename F>
-__device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_t base, int f) {
+__device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
   const int lane = threadIdx.x & 31;
   F v;
   int lv;
@@ -78,14 +79,14 @@ __device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_
     const int64_t i = base + 2 * lane;
     const F a = i < nvals ? __ldcg(vals + i) : F(0);
     const F b = i + 1 < nvals ? __ldcg(vals + i + 1) : F(0);
-    v = v1h(a, b);
+    v = top_node(a, b, cr);
     lv = 5;
   } else {
     const int64_t i = base + lane;
     v = (lane < (1 << f) && i < nvals) ? __ldcg(vals + i) : F(0);
     lv = f;
   }
-  for (int l = 0; l < lv; ++l) v = v1h(v, __shfl_xor_sync(0xffffffffu, v, 1 << l));
+  for (int l = 0; l < lv; ++l) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), cr);
   return v;
 }
 
@@ -112,7 +113,7 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
     if (old != expect - 1) return;
     __threadfence();  // acquire: the other arrivals' values are visible
     if (lane == 0) job.cnt[job.cnt_off[k] + g] = 0u;  // ready for the next call
-    const F v = warp_group_bal(job.vals + job.val_off[k], job.nin[k], g * fan, f);
+    const F v = warp_group_bal(job.vals + job.val_off[k], job.nin[k], g * fan, f, job.top_cr);
     if (k + 1 == job.nsteps) {
       if (lane == 0) *job.out = v;
       return;
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   unsigned pend_old = 0;
   for (int64_t grp = gw; grp < n_groups; grp += W) {
     F s0[1], s1[1], s2[1], gv[1];
-    NodeExact ne;
+    NodeTop ne{job.top_cr};
     for (int k = 0; k < G; k += NT) {  // rolled
       F tv[NT];
       const F* bases[NT];
@@ -344,8 +345,8 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
 // Balanced tree over vals[0..P) (entries >= nvals are +0) -> *out.  One CTA.
 template <typename F>
 __global__ void __launch_bounds__(kAuxThreads) bal_kernel(const F* vals, int64_t nvals, int64_t P,
-                                                       F* out) {
-  const F v = block_bal(vals, nvals, P);
+                                                       F* out, int cr) {
+  const F v = block_bal(vals, nvals, P, cr);
   if (threadIdx.x == 0) *out = v;
 }
 
@@ -355,12 +356,12 @@ __global__ void __launch_bounds__(kAuxThreads) bal_kernel(const F* vals, int64_t
 template <typename F>
 __global__ void __launch_bounds__(kAuxThreads) cols_combine_kernel(
     const F* vals, int64_t cols, int64_t tpc, int64_t p2c, F* col_norms, int64_t p2cols,
-    F* partials, unsigned* ticket, F* frob) {
+    F* partials, unsigned* ticket, F* frob, int cr) {
   __shared__ int s_last;
   const int64_t j = (int64_t)blockIdx.x * kAuxThreads + threadIdx.x;
   F v = F(0);
   if (j < cols) {
-    v = seq_bal(vals + j * tpc, tpc, 0, p2c);
+    v = seq_bal(vals + j * tpc, tpc, 0, p2c, cr);
     col_norms[j] = v;
   }
   if (frob == nullptr) return;
@@ -370,12 +371,12 @@ __global__ void __launch_bounds__(kAuxThreads) cols_combine_kernel(
   __shared__ F sh[kAuxWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wl = bl < 5 ? bl : 5;
-  for (int l = 0; l < wl; ++l) v = v1h(v, __shfl_xor_sync(0xffffffffu, v, 1 << l));
+  for (int l = 0; l < wl; ++l) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), cr);
   if (bl > 5) {
     if (lane == 0) sh[w] = v;
     __syncthreads();
     v = lane < kAuxWarps ? sh[lane] : F(0);
-    for (int l = 0; l < bl - 5; ++l) v = v1h(v, __shfl_xor_sync(0xffffffffu, v, 1 << l));
+    for (int l = 0; l < bl - 5; ++l) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), cr);
   }
   const int64_t pb = p2cols >> bl;  // values left after the block levels
   if (pb == 1) {
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(kAuxThreads) cols_combine_kernel(
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const F r = block_bal(partials, (int64_t)gridDim.x, pb);
+  const F r = block_bal(partials, (int64_t)gridDim.x, pb, cr);
   if (threadIdx.x == 0) {
     *frob = r;
     *ticket = 0u;
@@ -498,7 +499,7 @@ static int g_grid_override = 0;  // test hook: force a grid size (0 = automatic)
 template <typename F>
 static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int64_t len, int64_t p2,
                        F* tile_out, F* out, int combine, void* ws, size_t ws_bytes, bool vec,
-                       cudaStream_t s) {
+                       cudaStream_t s, int top_cr) {
   if (n_items == 0) return NRMF_OK;
   int64_t grid = (int64_t)device_sms() * (vec ? blocks_per_sm<F, true, NRMF_NT>() : blocks_per_sm<F, false, 1>());
   if (g_grid_override > 0) grid = g_grid_override;
@@ -525,6 +526,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   job.vals = reinterpret_cast<F*>(static_cast<char*>(ws) + cnt_bytes);
   job.out = out;
   job.combine = combine;
+  job.top_cr = top_cr;
   job.g0 = pl.g0;
   job.nsteps = pl.nsteps;
   for (int k = 0; k < kMaxSteps; ++k) {
@@ -548,7 +550,8 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
 }
 
 template <typename F>
-int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes, cudaStream_t s,
+              int top_cr) {
   // Evaluate the balanced tree over p2 tiles (p2 >= ceil(n/T), power of two)
   // of x[0..n) padded with +0; *out = root.  Caller validated arguments.
   const int64_t nt = (n + kTile - 1) / kTile;
@@ -557,32 +560,32 @@ int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_byt
     return NRMF_OK;
   }
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
-  return launch_tree<F>(x, nt, nt, 0, n, p2, nullptr, out, 1, ws, ws_bytes, vec, s);
+  return launch_tree<F>(x, nt, nt, 0, n, p2, nullptr, out, 1, ws, ws_bytes, vec, s, top_cr);
 }
 
-template int tree_eval<double>(int64_t, const double*, int64_t, double*, void*, size_t, cudaStream_t);
-template int tree_eval<float>(int64_t, const float*, int64_t, float*, void*, size_t, cudaStream_t);
+template int tree_eval<double>(int64_t, const double*, int64_t, double*, void*, size_t, cudaStream_t, int);
+template int tree_eval<float>(int64_t, const float*, int64_t, float*, void*, size_t, cudaStream_t, int);
 
 template <typename F>
-int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s) {
-  bal_kernel<F><<<1, kAuxThreads, 0, s>>>(vals, nvals, P, out);
+int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s, int top_cr) {
+  bal_kernel<F><<<1, kAuxThreads, 0, s>>>(vals, nvals, P, out, top_cr);
   return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
 }
-template int bal_eval<double>(const double*, int64_t, int64_t, double*, cudaStream_t);
-template int bal_eval<float>(const float*, int64_t, int64_t, float*, cudaStream_t);
+template int bal_eval<double>(const double*, int64_t, int64_t, double*, cudaStream_t, int);
+template int bal_eval<float>(const float*, int64_t, int64_t, float*, cudaStream_t, int);
 
 size_t tree_workspace(int64_t p2, size_t esz) { return tree_ws_bytes(p2, p2, esz); }
 
 // ---------------------------------------------------------------- vector
 template <typename F>
-static int nrmf_vec(int64_t n, const F* x, F* out, void* ws, size_t ws_bytes, void* stream) {
+static int nrmf_vec(int64_t n, const F* x, F* out, int flags, void* ws, size_t ws_bytes, void* stream) {
   if (n < 0 || out == nullptr || (n > 0 && (x == nullptr || ws == nullptr))) return NRMF_EINVAL;
   if ((reinterpret_cast<uintptr_t>(x) % sizeof(F)) != 0 ||
       (reinterpret_cast<uintptr_t>(out) % sizeof(F)) != 0)
     return NRMF_EALIGN;
   const int64_t nt = (n + kTile - 1) / kTile;
   return tree_eval<F>(n, x, pow2_ceil(std::max<int64_t>(nt, 1)), out, ws, ws_bytes,
-                      static_cast<cudaStream_t>(stream));
+                      static_cast<cudaStream_t>(stream), flags & NRMF_TOP_CR);
 }
 
 // ---------------------------------------------------------------- columns
@@ -600,7 +603,8 @@ static size_t cols_ws_bytes(int64_t rows, int64_t cols, size_t esz) {
 
 template <typename F>
 static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F* col_norms,
-                          F* frob, void* ws, size_t ws_bytes, void* stream) {
+                          F* frob, int flags, void* ws, size_t ws_bytes, void* stream) {
+  const int cr = flags & NRMF_TOP_CR;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (rows < 0 || cols < 0 || ld < rows || ld < 0) return NRMF_EINVAL;
   if (cols > 0 && col_norms == nullptr) return NRMF_EINVAL;
@@ -623,17 +627,17 @@ static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F*
   const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && ((ld * (int64_t)sizeof(F)) & 15) == 0;
   if (tpc == 1)
     return launch_tree<F>(A, cols, 1, ld, rows, p2cols, col_norms, frob, frob != nullptr ? 1 : 0, ws, ws_bytes,
-                          vec, s);
+                          vec, s, cr);
   unsigned* ticket = reinterpret_cast<unsigned*>(ws);
   char* base = static_cast<char*>(ws) + 256;
   F* vals = reinterpret_cast<F*>(base);
   F* partials = reinterpret_cast<F*>(base + align_up((size_t)(cols * tpc) * sizeof(F), 256));
-  int st = launch_tree<F>(A, cols * tpc, tpc, ld, rows, 1, vals, nullptr, 0, ws, ws_bytes, vec, s);
+  int st = launch_tree<F>(A, cols * tpc, tpc, ld, rows, 1, vals, nullptr, 0, ws, ws_bytes, vec, s, cr);
   if (st != NRMF_OK) return st;
   if (frob != nullptr && cudaMemsetAsync(ticket, 0, sizeof(unsigned), s) != cudaSuccess) return NRMF_ECUDA;
   const int64_t nblk = (cols + kAuxThreads - 1) / kAuxThreads;
   cols_combine_kernel<F><<<(unsigned)nblk, kAuxThreads, 0, s>>>(vals, cols, tpc, pow2_ceil(tpc), col_norms,
-                                                            p2cols, partials, ticket, frob);
+                                                            p2cols, partials, ticket, frob, cr);
   return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
 }
 
@@ -681,8 +685,9 @@ static size_t host_ws_bytes(int64_t n, size_t esz) {
 }
 
 template <typename F>
-static int nrmf_host_impl(int64_t n, const F* host_x, F* host_out, void* ws, size_t ws_bytes,
+static int nrmf_host_impl(int64_t n, const F* host_x, F* host_out, int flags, void* ws, size_t ws_bytes,
                           void* stream) {
+  const int cr = flags & NRMF_TOP_CR;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n < 0 || host_out == nullptr || ws == nullptr || (n > 0 && host_x == nullptr)) return NRMF_EINVAL;
   if (reinterpret_cast<uintptr_t>(host_x) % sizeof(F)) return NRMF_EALIGN;
@@ -723,12 +728,12 @@ static int nrmf_host_impl(int64_t n, const F* host_x, F* host_out, void* ws, siz
         return NRMF_ECUDA;
       if (cudaEventRecord(h->copied[slot], h->copy) != cudaSuccess) return NRMF_ECUDA;
       if (cudaStreamWaitEvent(s, h->copied[slot], 0) != cudaSuccess) return NRMF_ECUDA;
-      int st = tree_eval<F>(cnt, buf, c, nchunks == 1 ? dev_out : chunk_vals + k, tree_ws, tws, s);
+      int st = tree_eval<F>(cnt, buf, c, nchunks == 1 ? dev_out : chunk_vals + k, tree_ws, tws, s, cr);
       if (st != NRMF_OK) return st;
       if (cudaEventRecord(h->consumed[slot], s) != cudaSuccess) return NRMF_ECUDA;
     }
     if (nchunks > 1) {
-      int st = bal_eval<F>(chunk_vals, nchunks, p2 / c, dev_out, s);
+      int st = bal_eval<F>(chunk_vals, nchunks, p2 / c, dev_out, s, cr);
       if (st != NRMF_OK) return st;
     }
   }
@@ -779,19 +784,29 @@ size_t nrmf_workspace_bytes(int64_t n, int elem_bytes) {
   return tree_ws_bytes(nt, pow2_ceil(nt), (size_t)elem_bytes);
 }
 
+static bool flags_ok(int flags) { return (flags & ~NRMF_TOP_CR) == 0; }
+
 int nrmf_d(int64_t n, const double* x, double* out, void* ws, size_t ws_bytes, void* stream) {
-  return nrmf_vec<double>(n, x, out, ws, ws_bytes, stream);
+  return nrmf_vec<double>(n, x, out, 0, ws, ws_bytes, stream);
 }
 int nrmf_s(int64_t n, const float* x, float* out, void* ws, size_t ws_bytes, void* stream) {
-  return nrmf_vec<float>(n, x, out, ws, ws_bytes, stream);
+  return nrmf_vec<float>(n, x, out, 0, ws, ws_bytes, stream);
+}
+int nrmf_ex_d(int64_t n, const double* x, double* out, int flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!flags_ok(flags)) return NRMF_EINVAL;
+  return nrmf_vec<double>(n, x, out, flags, ws, ws_bytes, stream);
+}
+int nrmf_ex_s(int64_t n, const float* x, float* out, int flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!flags_ok(flags)) return NRMF_EINVAL;
+  return nrmf_vec<float>(n, x, out, flags, ws, ws_bytes, stream);
 }
 int nrmf_z_d(int64_t count, const double* z, double* out, void* ws, size_t ws_bytes, void* stream) {
   if (count < 0 || count > INT64_MAX / 2) return NRMF_EINVAL;
-  return nrmf_vec<double>(2 * count, z, out, ws, ws_bytes, stream);
+  return nrmf_vec<double>(2 * count, z, out, 0, ws, ws_bytes, stream);
 }
 int nrmf_z_s(int64_t count, const float* z, float* out, void* ws, size_t ws_bytes, void* stream) {
   if (count < 0 || count > INT64_MAX / 2) return NRMF_EINVAL;
-  return nrmf_vec<float>(2 * count, z, out, ws, ws_bytes, stream);
+  return nrmf_vec<float>(2 * count, z, out, 0, ws, ws_bytes, stream);
 }
 
 size_t nrmf_cols_workspace_bytes(int64_t rows, int64_t cols, int elem_bytes) {
@@ -800,11 +815,21 @@ size_t nrmf_cols_workspace_bytes(int64_t rows, int64_t cols, int elem_bytes) {
 }
 int nrmf_cols_d(int64_t rows, int64_t cols, int64_t ld, const double* A, double* col_norms,
                 double* frob, void* ws, size_t ws_bytes, void* stream) {
-  return nrmf_cols_impl<double>(rows, cols, ld, A, col_norms, frob, ws, ws_bytes, stream);
+  return nrmf_cols_impl<double>(rows, cols, ld, A, col_norms, frob, 0, ws, ws_bytes, stream);
 }
 int nrmf_cols_s(int64_t rows, int64_t cols, int64_t ld, const float* A, float* col_norms,
                 float* frob, void* ws, size_t ws_bytes, void* stream) {
-  return nrmf_cols_impl<float>(rows, cols, ld, A, col_norms, frob, ws, ws_bytes, stream);
+  return nrmf_cols_impl<float>(rows, cols, ld, A, col_norms, frob, 0, ws, ws_bytes, stream);
+}
+int nrmf_cols_ex_d(int64_t rows, int64_t cols, int64_t ld, const double* A, double* col_norms,
+                   double* frob, int flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!flags_ok(flags)) return NRMF_EINVAL;
+  return nrmf_cols_impl<double>(rows, cols, ld, A, col_norms, frob, flags, ws, ws_bytes, stream);
+}
+int nrmf_cols_ex_s(int64_t rows, int64_t cols, int64_t ld, const float* A, float* col_norms,
+                   float* frob, int flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!flags_ok(flags)) return NRMF_EINVAL;
+  return nrmf_cols_impl<float>(rows, cols, ld, A, col_norms, frob, flags, ws, ws_bytes, stream);
 }
 
 size_t nrmf_host_workspace_bytes(int64_t n, int elem_bytes) {
@@ -813,11 +838,21 @@ size_t nrmf_host_workspace_bytes(int64_t n, int elem_bytes) {
 }
 int nrmf_host_d(int64_t n, const double* host_x, double* host_out, void* ws, size_t ws_bytes,
                 void* stream) {
-  return nrmf_host_impl<double>(n, host_x, host_out, ws, ws_bytes, stream);
+  return nrmf_host_impl<double>(n, host_x, host_out, 0, ws, ws_bytes, stream);
 }
 int nrmf_host_s(int64_t n, const float* host_x, float* host_out, void* ws, size_t ws_bytes,
                 void* stream) {
-  return nrmf_host_impl<float>(n, host_x, host_out, ws, ws_bytes, stream);
+  return nrmf_host_impl<float>(n, host_x, host_out, 0, ws, ws_bytes, stream);
+}
+int nrmf_host_ex_d(int64_t n, const double* host_x, double* host_out, int flags, void* ws, size_t ws_bytes,
+                   void* stream) {
+  if (!flags_ok(flags)) return NRMF_EINVAL;
+  return nrmf_host_impl<double>(n, host_x, host_out, flags, ws, ws_bytes, stream);
+}
+int nrmf_host_ex_s(int64_t n, const float* host_x, float* host_out, int flags, void* ws, size_t ws_bytes,
+                   void* stream) {
+  if (!flags_ok(flags)) return NRMF_EINVAL;
+  return nrmf_host_impl<float>(n, host_x, host_out, flags, ws, ws_bytes, stream);
 }
 
 // test hook (not in nrmf.h): force the persistent grid size, 0 = automatic

@@ -103,7 +103,9 @@ size_t dist_ws(int64_t n, int world, size_t esz) {
 
 template <typename F>
 int dist_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, void* ws,
-              size_t ws_bytes, void* comm_v, void* stream) {
+              size_t ws_bytes, void* comm_v, void* stream, int flags) {
+  if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
+  const int cr = flags & NRMF_TOP_CR;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const NcclApi* api = nccl();
   if (api == nullptr) return NRMF_ENCCL;
@@ -132,7 +134,7 @@ int dist_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, void
 
   int st = NRMF_OK;
   if (p2l > 0 && cnt > 0) {
-    st = tree_eval<F>(cnt, x, p2l, local, tree_ws, tws, s);
+    st = tree_eval<F>(cnt, x, p2l, local, tree_ws, tws, s, cr);
   } else if (cudaMemsetAsync(local, 0, sizeof(F), s) != cudaSuccess) {
     st = NRMF_ECUDA;  // rank owns an all-padding subtree (value +0) or none
   }
@@ -141,7 +143,7 @@ int dist_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, void
   if (api->AllGather(local, gathered, 1, dt, comm, s) != ncclSuccess) return NRMF_ENCCL;
   // rank tree: the top levels over the ranks that own part of the tree
   const int64_t nr = std::min<int64_t>(world, P2);
-  return bal_eval<F>(gathered, nr, nr, out, s);
+  return bal_eval<F>(gathered, nr, nr, out, s, cr);
 }
 
 }  // namespace
@@ -165,11 +167,19 @@ size_t nrmf_dist_workspace_bytes(int64_t n_global, int world, int elem_bytes) {
 
 int nrmf_dist_d(int64_t n_global, int64_t offset, int64_t count, const double* x_local, double* out,
                 void* ws, size_t ws_bytes, void* nccl_comm, void* stream) {
-  return dist_impl<double>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream);
+  return dist_impl<double>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream, 0);
 }
 int nrmf_dist_s(int64_t n_global, int64_t offset, int64_t count, const float* x_local, float* out,
                 void* ws, size_t ws_bytes, void* nccl_comm, void* stream) {
-  return dist_impl<float>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream);
+  return dist_impl<float>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream, 0);
+}
+int nrmf_dist_ex_d(int64_t n_global, int64_t offset, int64_t count, const double* x_local, double* out,
+                   int flags, void* ws, size_t ws_bytes, void* nccl_comm, void* stream) {
+  return dist_impl<double>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream, flags);
+}
+int nrmf_dist_ex_s(int64_t n_global, int64_t offset, int64_t count, const float* x_local, float* out,
+                   int flags, void* ws, size_t ws_bytes, void* nccl_comm, void* stream) {
+  return dist_impl<float>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream, flags);
 }
 
 int nrmf_nccl_unique_id(char* id128) {

@@ -8,10 +8,11 @@
 namespace nrmf {
 // Balanced tree over p2 tiles of x[0..n) (zero padded) -> *out (device).
 template <typename F>
-int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes, cudaStream_t s);
+int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes, cudaStream_t s,
+              int top_cr);
 // Balanced tree over vals[0..P) (entries >= nvals are +0) -> *out, one CTA.
 template <typename F>
-int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s);
+int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s, int top_cr);
 // Workspace bytes of tree_eval for a p2-tile tree.
 size_t tree_workspace(int64_t p2, size_t esz);
 }  // namespace nrmf

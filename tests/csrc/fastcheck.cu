@@ -165,3 +165,17 @@ extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long 
   out3[0] = h.checked; out3[1] = h.fast; out3[2] = h.mism;
   return 0;
 }
+
+// cr_hypot (nrmf_crhypot.cuh) applied elementwise, for comparison with the
+// oracle's exact cr_hypot on the host.
+template <typename F>
+__global__ void crhypot_k(int64_t n, const F* a, const F* b, F* o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = cr_hypot(a[i], b[i]);
+}
+
+extern "C" int crhypot_array(int dbl, long long n, const void* a, const void* b, void* out) {
+  if (dbl) crhypot_k<double><<<148 * 4, 256>>>(n, (const double*)a, (const double*)b, (double*)out);
+  else crhypot_k<float><<<148 * 4, 256>>>(n, (const float*)a, (const float*)b, (float*)out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}

@@ -177,3 +177,33 @@ def test_no_spurious_overflow_or_underflow():
     assert oracle.v1_hypot(3 * t, 4 * t) == 5 * t
     # subnormal pair (inexact underflow regime): still nonzero
     assert oracle.v1_hypot(DMIN_SUB, DMIN_SUB) == DMIN_SUB
+
+
+@pytest.mark.parametrize("bits", [64, 32])
+def test_cr_hypot_is_exact_rounding(bits):
+    """oracle cr_hypot == RN(sqrt(x^2+y^2)) computed by the independent
+    exact-rational code (ieee_exact), incl. subnormal, huge and close pairs."""
+    dt = np.float64 if bits == 64 else np.float32
+    emin, emax = (-1074, 1020) if bits == 64 else (-149, 125)
+    n = 3000
+    xs = np.concatenate([rng.uniform(-2, 2, n), np.ldexp(rng.uniform(1, 2, n), rng.integers(emin, emax, n)),
+                         rng.integers(1, 1 << 20, n) * np.ldexp(1.0, emin)]).astype(dt)
+    ys = np.concatenate([rng.uniform(-2, 2, n), np.ldexp(rng.uniform(1, 2, n), rng.integers(emin, emax, n)),
+                         rng.integers(1, 1 << 20, n) * np.ldexp(1.0, emin)]).astype(dt)
+    ys[:500] = (xs[:500] * dt(1.0000001)).astype(dt)
+    got = oracle.cr_hypot_array(xs, ys)
+    for x, y, g in zip(xs, ys, got):
+        if not (math.isfinite(x) and math.isfinite(y)):
+            continue
+        assert ie.same(float(g), ie.exact_norm([float(x), float(y)], bits), bits)
+
+
+def test_cr_hypot_specials_and_closed_forms():
+    inf, nan = float("inf"), float("nan")
+    assert oracle.cr_hypot(3, 4) == 5 and oracle.cr_hypot(5, 12) == 13 and oracle.cr_hypot(8, 15) == 17
+    assert oracle.cr_hypot(1, 1) == math.sqrt(2.0)
+    assert oracle.cr_hypot(inf, nan) == inf and oracle.cr_hypot(nan, -inf) == inf
+    assert math.isnan(oracle.cr_hypot(nan, 1.0))
+    assert oracle.cr_hypot(-2.5, 0.0) == 2.5 and oracle.cr_hypot(0.0, 0.0) == 0.0
+    assert oracle.cr_hypot(1.5e308, 1.5e308) == inf and math.isfinite(oracle.cr_hypot(1.2e308, 1.2e308))
+    assert oracle.cr_hypot(DMAX, 1.0) == DMAX

@@ -254,3 +254,26 @@ def test_columns(dt):
     # empty shapes
     col3, frob3 = oracle.cols(np.zeros(0, dtype=dt), 0, 3, 0)
     assert np.all(col3 == 0) and frob3 == 0
+
+
+def test_A_top_reading_R1_f1():
+    """top="cr": Listing 1 with cr_hypot (A) above the tiles, v1
+    inside.  One tile: identical to the v1 tree.  e:r shape for A on n=7.
+    Shards + rank tree reproduce it.  Error within the A/H mixed bound."""
+    x = rng.uniform(-3, 3, 7)
+    C = lambda a, b: ie.exact_norm([float(a), float(b)])  # noqa: E731
+    exp = C(C(C(x[0], x[1]), C(x[2], x[3])), C(C(x[4], x[5]), abs(x[6])))
+    assert ie.same(float(oracle.R_A(x)), exp)
+    y = gen.normal(3, 4000)
+    assert oracle.nrmf(y, top="cr") == oracle.nrmf(y)           # no node above the single tile
+    z = gen.normal(4, 37 * T + 5)
+    a, v = oracle.nrmf(z, top="cr"), oracle.nrmf(z)
+    tiles = oracle.tiles(z)
+    assert a == oracle.combine(tiles, top="cr") and v == oracle.combine(tiles)
+    for G in (2, 4, 8):
+        assert oracle.combine_ranks(oracle.shard_norms(z, G, top="cr"), top="cr") == a
+    import mpmath
+    mpmath.mp.prec = 200
+    eps = mpmath.mpf(2) ** -53
+    ub = float(((oracle.reH_plus()) ** 12 * (1 + eps) ** 6 - 1) / eps)   # 12 v1 levels, 6 cr levels
+    assert oracle.relerr(a, oracle.exact(z)) <= ub
