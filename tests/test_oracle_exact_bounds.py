@@ -149,3 +149,50 @@ def test_extreme_range_variants_reading_R9():
         ex = oracle.exact(x)
         assert math.isfinite(ex)
         assert oracle.relerr(oracle.nrmf(x), ex) <= 64
+
+
+# --------------------------------------------------------------- SURVEY f4
+from oracle import bounds as B  # noqa: E402
+
+
+def test_table3_by_the_recurrences():
+    """Thm 1 (e:13) and Thm 3 (e:8, evaluated recursively over Listing 1's
+    tree with the clamp convention) reproduce all 90 printed values of
+    Table 3 to their 18 digits."""
+    for k, L, A, Hh in _golden():
+        n = 2 ** k
+        assert _sig18(B.bounds_L(n)[1], L), k
+        assert _sig18(B.bounds_R(n, "cr")[1], A), k
+        assert _sig18(B.bounds_R(n, "v1")[1], Hh), k
+
+
+def test_bounds_properties():
+    # lb <= 0 <= ub, growth laws (P:661-663): L doubles per doubling of n,
+    # A steps by 1 and H by ~3 per doubling
+    for k in range(10, 30):
+        n = 2 ** k
+        for lb, ub in (B.bounds_L(n), B.bounds_R(n, "cr"), B.bounds_R(n, "v1")):
+            assert lb <= 0 <= ub
+        assert 1.9 <= B.bounds_L(2 * n)[1] / B.bounds_L(n)[1] <= 2.1
+        assert abs(B.bounds_R(2 * n, "cr")[1] - B.bounds_R(n, "cr")[1] - 1) < 1e-6
+        assert abs(B.bounds_R(2 * n, "v1")[1] - B.bounds_R(n, "v1")[1] - 3) < 1e-6
+    # non-power-of-two n: Listing 1's ceil split, bound of ceil(lg n) levels
+    for n in (3, 5, 7, 1000, 12345):
+        d = (n - 1).bit_length()
+        assert abs(B.bounds_R(n, "v1")[1] - B.ub_depths(d)) < 1e-9
+
+
+def test_C_bound_about_twice_L():
+    """for large n the single-accumulator C bounds are about twice
+    those of L."""
+    for n in (2 ** 10, 2 ** 14):
+        r = float(B.bounds_C(n)[1] / B.bounds_L(n)[1])
+        assert 1.8 < r < 2.2
+
+
+def test_tile_tree_bound_f1():
+    """The A-style top makes the 64-eps target a theorem at n = 2^30 fp64
+    (SURVEY f1): 12 v1 levels + 18 cr levels -> 54 eps; all-v1 gives 90."""
+    assert abs(B.ub_depths(*B.tile_tree_depths(1 << 30)) - 90) < 1e-6
+    ub = B.ub_depths(*B.tile_tree_depths(1 << 30, top="cr"))
+    assert 53.9 < ub < 54.1 and ub < 64
