@@ -36,7 +36,7 @@ constexpr int kMaxSteps = 8;
 #define NRMF_USE_TMA 1        // 0: aligned full tiles use direct LDG.128 instead of the TMA ring
 #endif
 #ifndef NRMF_MIN_BLOCKS
-#define NRMF_MIN_BLOCKS 2     // CTAs per SM the register allocation must allow
+#define NRMF_MIN_BLOCKS 1     // CTAs per SM the register allocation must allow (16 warps x 128 registers)
 #endif
 constexpr int kStages = NRMF_STAGES;
 constexpr int kBPI = NRMF_BPI;
@@ -246,6 +246,71 @@ struct PipeLoader {
   }
 };
 
+// Vector-mode loader (ld == 0, 16-byte aligned x): the batches of a full
+// warp group (G consecutive full tiles, G*T contiguous elements) are
+// contiguous in memory, and a warp visits groups gw, gw+W, ...  The producer
+// is a pointer walk: +4 KiB per batch, +(W-1) groups at a group's end; it
+// stops at the first group that is not entirely full (the kernel reduces that
+// one, at most one per call, through single_tile).
+template <typename F>
+struct StreamLoader {
+  static constexpr int BPI = 1;
+  static constexpr bool kMaybePadding = false;
+  __device__ __forceinline__ bool all_padding(int) const { return false; }
+
+  uint32_t ring_s, bar_s;     // shared-window addresses of this warp's ring and barriers
+  uint32_t stash_s;           // this warp's stash (warp_tile_stash)
+  uint32_t consumed, issued;  // stages consumed / issued (warp-uniform)
+  const char* p_ptr;          // next batch to load
+  int64_t p_grp;              // its warp group
+  int p_left;                 // batches left in that group
+  int group_batches;          // G * J / kBatch
+  int64_t n_full;             // full warp groups
+  int64_t W;                  // warps in the grid
+  int64_t skip_bytes;         // (W - 1) groups
+  uint64_t policy;
+
+  __device__ __forceinline__ void issue() {
+    if (p_grp >= n_full) return;
+    if ((threadIdx.x & 31) == 0)
+      bulk_load(ring_s + (issued % kStages) * kBatchBytes, p_ptr, kBatchBytes, bar_s + (issued % kStages) * 8,
+                policy);
+    ++issued;
+    p_ptr += kBatchBytes;
+    if (--p_left == 0) {
+      p_left = group_batches;
+      p_grp += W;
+      p_ptr += skip_bytes;
+    }
+  }
+  __device__ __forceinline__ void begin(int) {
+    mbar_wait(bar_s + (consumed % kStages) * 8, (consumed / kStages) & 1);
+  }
+  __device__ __forceinline__ void get_row(int, int row, F (&o)[Cfg<F>::V]) const {
+    const uint32_t addr = ring_s + (consumed % kStages) * kBatchBytes + (threadIdx.x & 31) * 16 +
+                          row * (kBatchBytes / kBatch);
+    if constexpr (sizeof(F) == 8) {
+      double a0, a1;
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0), "=d"(a1) : "r"(addr) : "memory");
+      o[0] = a0;
+      o[1 % Cfg<F>::V] = a1;
+    } else {
+      float a0, a1, a2, a3;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3)
+                   : "r"(addr) : "memory");
+      o[0] = a0;
+      o[1 % Cfg<F>::V] = a1;
+      o[2 % Cfg<F>::V] = a2;
+      o[3 % Cfg<F>::V] = a3;
+    }
+  }
+  __device__ __forceinline__ void end(int) {
+    __syncwarp();  // every lane holds its leaves: the stage may be refilled
+    ++consumed;
+    issue();
+  }
+};
+
 // Value of tile tau when it is not part of a pipelined tuple: a full tile by
 // LDG (fast nodes, exact fallback), a partial one by the exact path, +0 for a
 // padding tile beyond the data.
@@ -258,18 +323,43 @@ __device__ __forceinline__ F single_tile(const TreeJob<F>& job, int64_t tau) {
   return warp_tile_exact<F, kPred>(tb, (int)remv);
 }
 
-template <typename F, bool TMA, int NT>
+template <typename F, bool TMA, int NT, bool STREAM>
 __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(const TreeJob<F> job) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr bool kPipe = TMA && NRMF_USE_TMA;
+  constexpr bool kStream = kPipe && STREAM && NT == 1;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + w;
   const int G = 1 << job.g0;
   const int64_t n_groups = (job.n_items + G - 1) >> job.g0;
+  // vector mode: groups made only of full tiles
+  const int64_t n_full = kStream ? (job.len / kTile) >> job.g0 : 0;
+
+  StreamLoader<F> sl;
+  if (kStream) {
+    sl.ring_s = smem_u32(smem + w * (kStages * kBatchBytes));
+    sl.bar_s = smem_u32(smem + kWarps * kStages * kBatchBytes) + w * kStages * 8;
+    sl.stash_s = smem_u32(smem + kWarps * kStages * kBatchBytes + 1024) + w * kStashBytes<F>;
+    if (lane == 0) {
+      for (int st = 0; st < kStages; ++st) mbar_init(sl.bar_s + st * 8, 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+    sl.consumed = sl.issued = 0;
+    sl.group_batches = G * (Cfg<F>::J / kBatch);
+    sl.p_left = sl.group_batches;
+    sl.p_grp = gw;
+    sl.n_full = n_full;
+    sl.W = W;
+    sl.p_ptr = reinterpret_cast<const char*>(job.x + gw * G * (int64_t)kTile);
+    sl.skip_bytes = (W - 1) * G * (int64_t)kTile * (int64_t)sizeof(F);
+    sl.policy = policy_evict_first();
+    for (int st = 0; st < kStages; ++st) sl.issue();
+  }
 
   PipeLoader<F, NT> pl;
-  if (kPipe) {
+  if (kPipe && !kStream) {
     pl.ring_s = smem_u32(smem + w * (kStages * kBatchBytes));
     pl.bar_s = smem_u32(smem + kWarps * kStages * kBatchBytes) + w * kStages * 8;
     if (lane == 0) {
@@ -301,7 +391,12 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     for (int k = 0; k < G; k += NT) {  // rolled
       F tv[NT];
       const F* bases[NT];
-      if (kPipe && pl.tuple_ok(grp, k, bases)) {
+      if (kStream && grp < n_full) {
+        NodeFast node;
+        tv[0] = warp_tile_stash<F>(sl, node, sl.stash_s);
+        if (__any_sync(0xffffffffu, node.bad) || tv[0] != tv[0])
+          tv[0] = warp_tile_exact<F, kVec>(job.x + (grp * G + k) * (int64_t)kTile, kTile);
+      } else if (kPipe && !kStream && pl.tuple_ok(grp, k, bases)) {
         NodeFast node;
         warp_tiles_impl<F, NT>(pl, node, tv);
         const bool bad = __any_sync(0xffffffffu, node.bad);
@@ -471,20 +566,24 @@ static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
 #define NRMF_NT 1             // tiles reduced in lockstep per warp when warp groups allow it
 #endif
 
+// [ring: kWarps x kStages x 4 KiB][barriers: 1 KiB][stash: kWarps x kStashBytes]
 template <typename F, bool TMA>
 static size_t kernel_smem() {
-  return (TMA && NRMF_USE_TMA) ? (size_t)kWarps * kStages * kBatchBytes + (size_t)kWarps * kStages * 8 : 0;
+  static_assert(kWarps * kStages * 8 <= 1024, "barrier area");
+  return (TMA && NRMF_USE_TMA) ? (size_t)kWarps * kStages * kBatchBytes + 1024 + (size_t)kWarps * kStashBytes<F>
+                               : 0;
 }
 
-template <typename F, bool TMA, int NT>
+template <typename F, bool TMA, int NT, bool STREAM>
 static int blocks_per_sm() {
   static int cached = 0;
   if (cached == 0) {
     const size_t sm = kernel_smem<F, TMA>();
     if (sm > 48 * 1024)
-      cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sm);
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT>, kThreads, sm) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM>, kThreads, sm) !=
             cudaSuccess ||
         b < 1)
       b = 1;
@@ -501,7 +600,10 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
                        F* tile_out, F* out, int combine, void* ws, size_t ws_bytes, bool vec,
                        cudaStream_t s, int top_cr) {
   if (n_items == 0) return NRMF_OK;
-  int64_t grid = (int64_t)device_sms() * (vec ? blocks_per_sm<F, true, NRMF_NT>() : blocks_per_sm<F, false, 1>());
+  const bool stream = vec && ld == 0;  // vector mode: contiguous warp groups
+  int64_t grid = (int64_t)device_sms() * (stream ? blocks_per_sm<F, true, 1, true>()
+                                          : vec  ? blocks_per_sm<F, true, NRMF_NT, false>()
+                                                 : blocks_per_sm<F, false, 1, false>());
   if (g_grid_override > 0) grid = g_grid_override;
   // warp groups of up to 8 tiles while there is enough work for every warp
   int g0_max = 0;
@@ -537,14 +639,16 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   }
   const int64_t n_groups = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
   grid = std::min<int64_t>(grid, (n_groups + kWarps - 1) / kWarps);
-  if (vec && pl.g0 >= 1 && NRMF_NT == 2) {
-    blocks_per_sm<F, true, NRMF_NT>();
-    nrmf_tree_kernel<F, true, NRMF_NT><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
+  if (stream) {
+    nrmf_tree_kernel<F, true, 1, true><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
+  } else if (vec && pl.g0 >= 1 && NRMF_NT == 2) {
+    blocks_per_sm<F, true, NRMF_NT, false>();
+    nrmf_tree_kernel<F, true, NRMF_NT, false><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
   } else if (vec) {
-    blocks_per_sm<F, true, 1>();
-    nrmf_tree_kernel<F, true, 1><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
+    blocks_per_sm<F, true, 1, false>();
+    nrmf_tree_kernel<F, true, 1, false><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
   } else {
-    nrmf_tree_kernel<F, false, 1><<<(unsigned)grid, kThreads, kernel_smem<F, false>(), s>>>(job);
+    nrmf_tree_kernel<F, false, 1, false><<<(unsigned)grid, kThreads, kernel_smem<F, false>(), s>>>(job);
   }
   return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
 }

@@ -145,6 +145,72 @@ __global__ void check_sqrt_d(uint64_t seed, uint64_t n, Counts* c) {
   atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
 }
 
+// Internal (unchecked) nodes: operands >= +0 with the larger one M anywhere
+// in the fast domain [2^-900, 2^1021) (fp64) / [2^-80, 2^125) (fp32) -- the
+// range DESIGN.md §7 shows every internal node of a tile lies in once its leaf
+// nodes passed their check.  m is arbitrary in [0, M] (zero, subnormal, q < 2^-69,
+// q near 1).  Every pair must equal the exact node; `fast` counts in-domain pairs.
+__global__ void check_internal_d(uint64_t seed, uint64_t n, Counts* c) {
+  unsigned long long ck = 0, fa = 0, mi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    const int eM = (int)(mix(k) % 1921) - 900;                       // [2^-900, 2^1021)
+    const double M = ldexp(1.0 + (double)(k >> 12) * 0x1p-52, eM);
+    const uint64_t k2 = mix(k + 1);
+    double m;
+    switch (k2 & 3) {
+      case 0: m = ldexp(1.0 + (double)(mix(k2) >> 12) * 0x1p-52, eM - (int)(mix(k2 + 1) % 3)); break;  // q ~ 1
+      case 1: m = ldexp(1.0 + (double)(mix(k2) >> 12) * 0x1p-52, eM - (int)(mix(k2 + 1) % 120)); break;
+      case 2: m = ldexp(1.0 + (double)(mix(k2) >> 12) * 0x1p-52, (int)(mix(k2 + 1) % 2098) - 1074); break;
+      default: m = __longlong_as_double((long long)(mix(k2) & ((1ull << 52) - 1)) * ((k2 >> 2) & 1)); break;  // subnormal / 0
+    }
+    if (m > M) m = M;  // keep M the larger operand
+    const double a[1] = {(k2 & 4) ? M : m}, b[1] = {(k2 & 4) ? m : M};
+    double h[1];
+    bool bad = false;
+    v1h_fast_n<false, 1>(a, b, h, bad);
+    ++ck;
+    const bool in = (unsigned)__double2hiint(fmax(a[0], b[0])) - kFastLoD < kFastSpanD;
+    if (in) {
+      ++fa;
+      if (__double_as_longlong(h[0]) != __double_as_longlong(v1h(a[0], b[0]))) ++mi;
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
+}
+
+__global__ void check_internal_s(uint64_t seed, uint64_t n, Counts* c) {
+  unsigned long long ck = 0, fa = 0, mi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    const int eM = (int)(mix(k) % 205) - 80;                          // [2^-80, 2^125)
+    const float M = ldexpf(1.0f + (float)(k >> 41) * 0x1p-23f, eM);
+    const uint64_t k2 = mix(k + 1);
+    float m;
+    switch (k2 & 3) {
+      case 0: m = ldexpf(1.0f + (float)(mix(k2) >> 41) * 0x1p-23f, eM - (int)(mix(k2 + 1) % 3)); break;
+      case 1: m = ldexpf(1.0f + (float)(mix(k2) >> 41) * 0x1p-23f, eM - (int)(mix(k2 + 1) % 40)); break;
+      case 2: m = ldexpf(1.0f + (float)(mix(k2) >> 41) * 0x1p-23f, (int)(mix(k2 + 1) % 277) - 149); break;
+      default: m = __int_as_float((int)(mix(k2) & ((1u << 23) - 1)) * (int)((k2 >> 2) & 1)); break;
+    }
+    if (m > M) m = M;
+    // packed pair (FFMA2 path): (a, b) and (b, a)
+    const float a[2] = {(k2 & 4) ? M : m, (k2 & 4) ? m : M}, b[2] = {(k2 & 4) ? m : M, (k2 & 4) ? M : m};
+    float h[2];
+    bool bad = false;
+    v1h_fast_n<false, 2>(a, b, h, bad);
+    ++ck;
+    const bool in = (unsigned)__float_as_int(fmaxf(a[0], b[0])) - kFastLoS < kFastSpanS;
+    if (in) {
+      ++fa;
+      const float e = v1h(a[0], b[0]);
+      if (__float_as_int(h[0]) != __float_as_int(e)) ++mi;
+      if (__float_as_int(h[1]) != __float_as_int(e)) ++mi;
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
+}
+
 extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long n, int mode,
                          unsigned long long* out3) {
   Counts* c;
@@ -156,6 +222,8 @@ extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long 
     case 2: check_sqrt_s_exhaustive<<<148 * 8, 256>>>(c); break;
     case 3: check_div_s<<<dim3(64, 2048), 256>>>((uint32_t)n, c); break;
     case 4: check_sqrt_d<<<148 * 8, 256>>>(seed, n, c); break;
+    case 5: check_internal_d<<<148 * 8, 256>>>(seed, n, c); break;
+    case 6: check_internal_s<<<148 * 8, 256>>>(seed, n, c); break;
     default: return 2;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return 3;

@@ -70,3 +70,14 @@ def test_fp32_div_exhaustive(fc):
 def test_fp64_sqrt_random_and_near_midpoints(fc):
     checked, _, mism = fc(4, seed=5, n=1 << 30)
     assert checked == 1 << 30 and mism == 0
+
+
+@pytest.mark.parametrize("which", [5, 6], ids=["fp64", "fp32"])
+def test_internal_node_unchecked_in_fast_domain(fc, which):
+    """Internal nodes of a tile run without a range check: in
+    the whole fast domain of M -- which the leaf check plus the 12-level growth
+    bound guarantees for every internal node -- the unchecked fast node equals
+    the exact node bit for bit, for any 0 <= m <= M (q near 1, tiny q,
+    subnormal and zero m)."""
+    checked, fast, mism = fc(which, seed=31 + which, n=1 << 28)
+    assert checked == 1 << 28 and fast == checked and mism == 0

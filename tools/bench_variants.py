@@ -5,8 +5,10 @@
 Inputs are random normal data generated on the device (timing only; parity
 is the tests' job).  CUDA-event timing, 2^30 elements, median of 20 reps."""
 import ctypes
+import os
 import statistics
 import sys
+import time
 
 import torch
 
@@ -21,6 +23,39 @@ def load(path):
     return L
 
 
+class Clock:
+    """NVML SM-clock sampler (MHz) running while the context is open."""
+
+    def __init__(self):
+        import threading
+        import pynvml as nv
+        nv.nvmlInit()
+        self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        self.samples, self.stop, self.threading = [], None, threading
+
+    def __enter__(self):
+        self.samples = []
+        self.stop = self.threading.Event()
+
+        def run():
+            while not self.stop.is_set():
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                time.sleep(0.002)
+        self.t = self.threading.Thread(target=run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join()
+
+    def mhz(self):
+        return statistics.mean(self.samples) if self.samples else float("nan")
+
+
+CLK = None
+
+
 def time_one(L, x, reps=20):
     n = x.numel()
     esz = x.element_size()
@@ -32,23 +67,43 @@ def time_one(L, x, reps=20):
     for _ in range(3):
         assert call() == 0
     ts = []
-    for _ in range(reps):
-        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(); call(); e1.record(); torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
+    global CLK
+    if CLK is None:
+        CLK = Clock()
+    with CLK:
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(); call(); e1.record(); torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+    # time normalised to the 1965 MHz max clock (compute-bound kernels scale with the clock)
+    time_one.last_mhz = CLK.mhz()
     return statistics.median(ts), out.item()
 
 
 def main():
+    """Variants are timed in interleaved rounds (A B C A B C ...) so that a
+    drift of the SM clock over the run (power/thermal) hits all of them alike;
+    the report is the per-variant minimum and median over rounds."""
     n = 1 << 30
+    rounds = int(os.environ.get("ROUNDS", "3"))
     xd = torch.randn(n, dtype=torch.float64, device="cuda")
     xs = torch.randn(n, dtype=torch.float32, device="cuda") * 3
-    for p in sys.argv[1:]:
-        L = load(p)
-        td, rd = time_one(L, xd)
-        ts, rs = time_one(L, xs)
-        print(f"{p}: fp64 {td:.4f} ms ({n*8/td/1e6:.0f} GB/s) r={rd!r}  fp32 {ts:.4f} ms ({n*4/ts/1e6:.0f} GB/s) r={rs!r}",
-              flush=True)
+    libs = [(p, load(p)) for p in sys.argv[1:]]
+    res = {p: ([], [], [], [], None, None) for p, _ in libs}
+    for _ in range(rounds):
+        for p, L in libs:
+            td, rd = time_one(L, xd, reps=10)
+            cd = time_one.last_mhz
+            ts, rs = time_one(L, xs, reps=10)
+            cs = time_one.last_mhz
+            d, f, nd, nf, _, _ = res[p]
+            d.append(td); f.append(ts); nd.append(td * cd / 1965.0); nf.append(ts * cs / 1965.0)
+            res[p] = (d, f, nd, nf, rd, rs)
+    for p, _ in libs:
+        d, f, nd, nf, rd, rs = res[p]
+        print(f"{p}: fp64 min {min(d):.4f} med {statistics.median(d):.4f} ms @1965-norm {statistics.median(nd):.4f} | "
+              f"fp32 min {min(f):.4f} med {statistics.median(f):.4f} ms @1965-norm {statistics.median(nf):.4f} "
+              f"| r={rd!r} {rs!r}", flush=True)
 
 
 
