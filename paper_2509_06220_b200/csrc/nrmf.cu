@@ -259,7 +259,8 @@ struct StreamLoader {
   __device__ __forceinline__ bool all_padding(int) const { return false; }
 
   uint32_t ring_s, bar_s;     // shared-window addresses of this warp's ring and barriers
-  uint32_t stash_s;           // this warp's stash (warp_tile_stash)
+  uint32_t stash_s;           // this warp's stash (warp_tile_lanes)
+  uint32_t xs_s;              // this warp's thread values of a warp group (group_cross)
   uint32_t consumed, issued;  // stages consumed / issued (warp-uniform)
   const char* p_ptr;          // next batch to load
   int64_t p_grp;              // its warp group
@@ -341,6 +342,8 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     sl.ring_s = smem_u32(smem + w * (kStages * kBatchBytes));
     sl.bar_s = smem_u32(smem + kWarps * kStages * kBatchBytes) + w * kStages * 8;
     sl.stash_s = smem_u32(smem + kWarps * kStages * kBatchBytes + 1024) + w * kStashBytes<F>;
+    sl.xs_s = smem_u32(smem + kWarps * kStages * kBatchBytes + 1024 + kWarps * kStashBytes<F>) +
+              w * kGroupXsBytes<F>;
     if (lane == 0) {
       for (int st = 0; st < kStages; ++st) mbar_init(sl.bar_s + st * 8, 1);
       fence_mbar_init();
@@ -388,15 +391,33 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   for (int64_t grp = gw; grp < n_groups; grp += W) {
     F s0[1], s1[1], s2[1], gv[1];
     NodeTop ne{job.top_cr};
-    for (int k = 0; k < G; k += NT) {  // rolled
+    bool group_done = false;
+    if (kStream && grp < n_full) {
+      // full warp group of a vector call: per tile the thread values go to
+      // the warp's xs area, then the cross-thread and group levels of all G
+      // tiles at once (group_cross).  A flagged leaf or a NaN tile value
+      // recomputes the group with the exact path below.
+      NodeFast node;
+      for (int k = 0; k < G; ++k) {  // rolled
+        const F c = warp_tile_lanes<F>(sl, node, sl.stash_s);
+        st_shared(sl.xs_s + (k * 32 + lane) * (uint32_t)sizeof(F), c);
+      }
+      __syncwarp();
+      if (!__any_sync(0xffffffffu, node.bad)) group_done = group_cross<F>(node, sl.xs_s, G, job.top_cr, gv[0]);
+      if (!group_done) {
+        for (int k = 0; k < G; ++k) {  // rolled
+          gv[0] = warp_tile_exact<F, kVec>(job.x + (grp * G + k) * (int64_t)kTile, kTile);
+          if (G == 8) counter_merge<F, 1, 8>(k, gv, s0, s1, s2, ne);
+          else if (G == 4) counter_merge<F, 1, 4>(k, gv, s0, s1, s2, ne);
+          else if (G == 2) counter_merge<F, 1, 2>(k, gv, s0, s1, s2, ne);
+        }
+        group_done = true;
+      }
+    }
+    for (int k = 0; k < G && !group_done; k += NT) {  // rolled
       F tv[NT];
       const F* bases[NT];
-      if (kStream && grp < n_full) {
-        NodeFast node;
-        tv[0] = warp_tile_stash<F>(sl, node, sl.stash_s);
-        if (__any_sync(0xffffffffu, node.bad) || tv[0] != tv[0])
-          tv[0] = warp_tile_exact<F, kVec>(job.x + (grp * G + k) * (int64_t)kTile, kTile);
-      } else if (kPipe && !kStream && pl.tuple_ok(grp, k, bases)) {
+      if (kPipe && !kStream && pl.tuple_ok(grp, k, bases)) {
         NodeFast node;
         warp_tiles_impl<F, NT>(pl, node, tv);
         const bool bad = __any_sync(0xffffffffu, node.bad);
@@ -567,10 +588,12 @@ static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
 #endif
 
 // [ring: kWarps x kStages x 4 KiB][barriers: 1 KiB][stash: kWarps x kStashBytes]
+// [xs: kWarps x 8 tiles x 32 thread values]
 template <typename F, bool TMA>
 static size_t kernel_smem() {
   static_assert(kWarps * kStages * 8 <= 1024, "barrier area");
-  return (TMA && NRMF_USE_TMA) ? (size_t)kWarps * kStages * kBatchBytes + 1024 + (size_t)kWarps * kStashBytes<F>
+  return (TMA && NRMF_USE_TMA) ? (size_t)kWarps * kStages * kBatchBytes + 1024 +
+                                     (size_t)kWarps * (kStashBytes<F> + kGroupXsBytes<F>)
                                : 0;
 }
 
