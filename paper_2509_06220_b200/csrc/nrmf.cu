@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -629,8 +630,25 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
                                                  : blocks_per_sm<F, false, 1, false>());
   if (g_grid_override > 0) grid = g_grid_override;
   // warp groups of up to 8 tiles while there is enough work for every warp
+  // Warp-group size 2^g0 (<= 8 tiles).  The persistent warps take groups
+  // round-robin, so the makespan is ceil(groups / W) groups of G tiles, and a
+  // group costs about G + 1/3 tiles (its cross-thread tail, announce and
+  // climb; measured at n = 2^26 / 2^28).  Take the G minimising
+  // ceil(groups / W) * (G + 1/3), the larger on ties.  The tree does not
+  // depend on g0.
   int g0_max = 0;
-  while (g0_max < 3 && n_items >= (int64_t(2) << g0_max) * grid * kWarps) ++g0_max;
+  {
+    const int64_t W = grid * kWarps;
+    double best = 0.0;
+    for (int g = 3; g >= 0; --g) {
+      const int64_t groups = (n_items + (int64_t(1) << g) - 1) >> g;
+      const double cost = (double)((groups + W - 1) / W) * ((double)(1 << g) + 1.0 / 3.0);
+      if (g == 3 || cost < best - 1e-9) {
+        best = cost;
+        g0_max = g;
+      }
+    }
+  }
   const Plan pl = combine ? make_plan(n_items, p2, g0_max) : make_plan(n_items, 1, 0);
   const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
   const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
