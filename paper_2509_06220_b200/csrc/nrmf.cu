@@ -62,6 +62,7 @@ struct TreeJob {
   int combine;         // 0: only write tile values
   int top_cr;          // levels above the tiles use cr_hypot (NRMF_TOP_CR)
   int g0;              // tile-tree levels combined inside a warp group (<= 3)
+  int cta_minor;       // warp index w * gridDim + block (few groups) instead of block * kWarps + w
   int nsteps;          // combine steps above the warp groups
   int lg_fan[kMaxSteps];
   int64_t nin[kMaxSteps];      // real (non-padding) inputs of step k (nin[0] = warp groups)
@@ -332,7 +333,10 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   constexpr bool kStream = kPipe && STREAM && NT == 1;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * kWarps;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + w;
+  // global warp index: CTA-major (a CTA streams kWarps consecutive groups)
+  // when every warp has work; CTA-minor for calls with fewer groups than
+  // warps, so that consecutive groups go to different SMs
+  const int64_t gw = job.cta_minor ? (int64_t)w * gridDim.x + blockIdx.x : (int64_t)blockIdx.x * kWarps + w;
   const int G = 1 << job.g0;
   const int64_t n_groups = (job.n_items + G - 1) >> job.g0;
   // vector mode: groups made only of full tiles
@@ -679,7 +683,8 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
     job.cnt_off[k] = pl.cnt_off[k];
   }
   const int64_t n_groups = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
-  grid = std::min<int64_t>(grid, (n_groups + kWarps - 1) / kWarps);
+  job.cta_minor = n_groups < grid * kWarps;
+  grid = std::min<int64_t>(grid, n_groups);
   if (stream) {
     nrmf_tree_kernel<F, true, 1, true><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
   } else if (vec && pl.g0 >= 1 && NRMF_NT == 2) {
