@@ -1,0 +1,96 @@
+"""CUDA-graph capture of nrmf calls (kernel, allgather and rank
+tree captured once, replayed with one launch): replays give the oracle's bits,
+including after the input changes in place between replays."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import nrmf_inputs as gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+T = 4096
+
+
+@pytest.fixture(scope="module")
+def nrmf():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2509_06220_b200 import _build
+    _build.build()
+    import paper_2509_06220_b200 as m
+    m.lib()
+    torch.cuda.set_device(0)
+    return m
+
+
+def bits(v, dt):
+    return np.asarray(v, dtype=dt).tobytes()
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("n", [5, 3 * T + 7, 300 * T + 11])
+def test_norm_graph_replay(nrmf, dt, n):
+    x1 = gen.normal(7, n, dtype=dt)
+    x2 = gen.sme(8, n, dtype=dt)
+    x = torch.from_numpy(x1).cuda()
+    out = torch.empty((), dtype=x.dtype, device="cuda")
+    g = nrmf.capture(lambda: nrmf.norm(x, out=out))
+    for _ in range(3):
+        g.replay()
+        torch.cuda.synchronize()
+        assert bits(out.cpu().numpy(), dt) == bits(oracle.nrmf(x1), dt)
+    x.copy_(torch.from_numpy(x2))          # same buffer, new contents
+    g.replay()
+    torch.cuda.synchronize()
+    assert bits(out.cpu().numpy(), dt) == bits(oracle.nrmf(x2), dt)
+
+
+def test_cols_graph_replay(nrmf):
+    r, c = 4096 + 5, 37
+    A = gen.normal(9, r * c, dtype=np.float64).reshape(c, r)    # column j = row j of this array
+    At = torch.from_numpy(A).cuda().t()                           # column-major view
+    col = torch.empty(c, dtype=torch.float64, device="cuda")
+    fr = torch.empty((), dtype=torch.float64, device="cuda")
+
+    def call():
+        cc, ff = nrmf.cols(At)
+        col.copy_(cc)
+        fr.copy_(ff)
+    g = nrmf.capture(call)
+    g.replay()
+    torch.cuda.synchronize()
+    got = col.cpu().numpy()
+    for j in range(c):
+        assert bits(got[j], np.float64) == bits(oracle.nrmf(A[j]), np.float64)
+
+
+def test_dist_graph_replay_world1(nrmf):
+    """nrmf.dist (tree kernel + ncclAllGather + rank tree) captured on a
+    1-rank NCCL communicator: replays equal the oracle bitwise."""
+    import torch.distributed as td
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29541")
+    created = False
+    if not td.is_initialized():
+        td.init_process_group("gloo", rank=0, world_size=1)
+        created = True
+    try:
+        for dt in (np.float64, np.float32):
+            n = 100 * T + 5
+            xh = gen.normal(3, n, dtype=dt)
+            x = torch.from_numpy(xh).cuda()
+            out = torch.empty((), dtype=x.dtype, device="cuda")
+            comm = nrmf.comm_for(None)
+            g = nrmf.capture(lambda: nrmf.dist(x, n, comm=comm, out=out))
+            for _ in range(2):
+                g.replay()
+                torch.cuda.synchronize()
+                assert bits(out.cpu().numpy(), dt) == bits(oracle.nrmf(xh), dt)
+    finally:
+        for c in list(nrmf._comms.values()):
+            c.close()
+        nrmf._comms.clear()
+        if created:
+            td.destroy_process_group()
