@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   const int G = 1 << job.g0;
   const int64_t n_groups = (job.n_items + G - 1) >> job.g0;
   // vector mode: groups made only of full tiles
-  const int64_t n_full = kStream ? (job.len / kTile) >> job.g0 : 0;
+  // stream mode: warp groups made only of full tiles (tiles are contiguous:
+  // a vector, or columns with ld == rows == a multiple of T)
+  const int64_t n_full = kStream ? (job.ld == 0 ? job.len / kTile : job.n_items) >> job.g0 : 0;
 
   StreamLoader<F> sl;
   if (kStream) {
@@ -408,10 +410,13 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         st_shared(sl.xs_s + (k * 32 + lane) * (uint32_t)sizeof(F), c);
       }
       __syncwarp();
-      if (!__any_sync(0xffffffffu, node.bad)) group_done = group_cross<F>(node, sl.xs_s, G, job.top_cr, gv[0]);
+      if (!__any_sync(0xffffffffu, node.bad))
+        group_done = group_cross<F>(node, sl.xs_s, G, job.top_cr, gv[0],
+                                    job.tile_out != nullptr ? job.tile_out + grp * G : nullptr);
       if (!group_done) {
         for (int k = 0; k < G; ++k) {  // rolled
           gv[0] = warp_tile_exact<F, kVec>(job.x + (grp * G + k) * (int64_t)kTile, kTile);
+          if (job.tile_out != nullptr && lane == 0) job.tile_out[grp * G + k] = gv[0];
           if (G == 8) counter_merge<F, 1, 8>(k, gv, s0, s1, s2, ne);
           else if (G == 4) counter_merge<F, 1, 4>(k, gv, s0, s1, s2, ne);
           else if (G == 2) counter_merge<F, 1, 2>(k, gv, s0, s1, s2, ne);
@@ -628,7 +633,9 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
                        F* tile_out, F* out, int combine, void* ws, size_t ws_bytes, bool vec,
                        cudaStream_t s, int top_cr) {
   if (n_items == 0) return NRMF_OK;
-  const bool stream = vec && ld == 0;  // vector mode: contiguous warp groups
+  // contiguous tiles (a vector, or whole columns of T-multiple length stored
+  // back to back): warp groups are contiguous, the pointer-walk producer applies
+  const bool stream = vec && (ld == 0 || (ld == len && len % kTile == 0));
   int64_t grid = (int64_t)device_sms() * (stream ? blocks_per_sm<F, true, 1, true>()
                                           : vec  ? blocks_per_sm<F, true, NRMF_NT, false>()
                                                  : blocks_per_sm<F, false, 1, false>());
@@ -653,7 +660,10 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
       }
     }
   }
-  const Plan pl = combine ? make_plan(n_items, p2, g0_max) : make_plan(n_items, 1, 0);
+  // without a combine (tile values only) the warp groups still batch the
+  // cross-thread levels of their tiles; their group value is not used
+  const Plan pl = combine ? make_plan(n_items, p2, g0_max)
+                          : make_plan(n_items, int64_t(1) << g0_max, g0_max);
   const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
   const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
   if (combine && ws_bytes < need) return NRMF_EWORKSPACE;

@@ -298,3 +298,15 @@ def test_c5_extreme_2p27(nrmf, variant):
         assert ex == np.inf and r == np.inf
     else:
         assert math.isfinite(ex) and oracle.relerr(r, ex) <= 64
+
+
+@pytest.mark.slow
+def test_max_size_beyond_2p31_elements(nrmf):
+    """Maximum-size edge case: n = 2^31 + 3*4096 + 5 fp32 elements (8 GiB): element
+    indices beyond 2^31 and a ragged tail in a 2^20-tile tree (P2 = 2^20 with
+    2^19 + 4 real tiles); bit-exact with the oracle over the whole array."""
+    n = (1 << 31) + 3 * T + 5
+    x = gen.sme(3, n)
+    r = gpu_norm(nrmf, x)
+    assert bits(r, np.float32) == bits(oracle.nrmf(x), np.float32)
+    torch.cuda.empty_cache()
