@@ -248,49 +248,58 @@ struct PipeLoader {
   }
 };
 
-// Vector-mode loader (ld == 0, 16-byte aligned x): the batches of a full
-// warp group (G consecutive full tiles, G*T contiguous elements) are
-// contiguous in memory, and a warp visits groups gw, gw+W, ...  The producer
-// is a pointer walk: +4 KiB per batch, +(W-1) groups at a group's end; it
-// stops at the first group that is not entirely full (the kernel reduces that
-// one, at most one per call, through single_tile).
+// Per-warp shared-memory block of the stream kernel (offsets from its base):
+// [ring: kStages x 4 KiB][stash][group thread values][mbarriers], 128-aligned.
+template <typename F>
+struct WarpSmem {
+  static constexpr uint32_t kRing = 0;
+  static constexpr uint32_t kStash = kStages * kBatchBytes;
+  static constexpr uint32_t kXs = kStash + kStashBytes<F>;
+  static constexpr uint32_t kBars = kXs + kGroupXsBytes<F>;
+  static constexpr uint32_t kBytes = (kBars + kStages * 8 + 127) / 128 * 128;
+};
+
+// Stream loader (contiguous tiles: a vector, or back-to-back columns of T
+// multiple length; 16-byte aligned): the batches of a full warp group (G
+// consecutive full tiles, G*T contiguous elements) are contiguous in memory,
+// and a warp visits groups gw, gw+W, ...  The producer is a pointer walk:
+// +4 KiB per batch, +(W-1) groups at a group's end; it stops after the warp's
+// last full group (a partial last group of the call goes through
+// single_tile).  Every consumed stage is refilled at once, so the slot to fill
+// is always the one just consumed.  State: 5 registers plus kernel-uniform
+// values.
 template <typename F>
 struct StreamLoader {
   static constexpr int BPI = 1;
   static constexpr bool kMaybePadding = false;
   __device__ __forceinline__ bool all_padding(int) const { return false; }
+  using L = WarpSmem<F>;
 
-  uint32_t ring_s, bar_s;     // shared-window addresses of this warp's ring and barriers
-  uint32_t stash_s;           // this warp's stash (warp_tile_lanes)
-  uint32_t xs_s;              // this warp's thread values of a warp group (group_cross)
-  uint32_t consumed, issued;  // stages consumed / issued (warp-uniform)
-  const char* p_ptr;          // next batch to load
-  int64_t p_grp;              // its warp group
-  int p_left;                 // batches left in that group
-  int group_batches;          // G * J / kBatch
-  int64_t n_full;             // full warp groups
-  int64_t W;                  // warps in the grid
-  int64_t skip_bytes;         // (W - 1) groups
-  uint64_t policy;
+  uint32_t my_s;         // this warp's block (WarpSmem)
+  uint32_t consumed;     // stages consumed (warp-uniform)
+  const char* p_ptr;     // next batch to load
+  int p_left;            // batches left in its group
+  int groups_left;       // further groups after it (-1: nothing left to load)
+  int group_batches;     // G * J / kBatch            (kernel-uniform)
+  int64_t skip_bytes;    // (W - 1) groups in bytes   (kernel-uniform)
 
-  __device__ __forceinline__ void issue() {
-    if (p_grp >= n_full) return;
+  __device__ __forceinline__ void issue(uint32_t slot) {
+    if (groups_left < 0) return;
     if ((threadIdx.x & 31) == 0)
-      bulk_load(ring_s + (issued % kStages) * kBatchBytes, p_ptr, kBatchBytes, bar_s + (issued % kStages) * 8,
-                policy);
-    ++issued;
+      bulk_load(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
+                policy_evict_first());
     p_ptr += kBatchBytes;
     if (--p_left == 0) {
       p_left = group_batches;
-      p_grp += W;
       p_ptr += skip_bytes;
+      --groups_left;
     }
   }
   __device__ __forceinline__ void begin(int) {
-    mbar_wait(bar_s + (consumed % kStages) * 8, (consumed / kStages) & 1);
+    mbar_wait(my_s + L::kBars + (consumed % kStages) * 8, (consumed / kStages) & 1);
   }
   __device__ __forceinline__ void get_row(int, int row, F (&o)[Cfg<F>::V]) const {
-    const uint32_t addr = ring_s + (consumed % kStages) * kBatchBytes + (threadIdx.x & 31) * 16 +
+    const uint32_t addr = my_s + L::kRing + (consumed % kStages) * kBatchBytes + (threadIdx.x & 31) * 16 +
                           row * (kBatchBytes / kBatch);
     if constexpr (sizeof(F) == 8) {
       double a0, a1;
@@ -309,8 +318,9 @@ struct StreamLoader {
   }
   __device__ __forceinline__ void end(int) {
     __syncwarp();  // every lane holds its leaves: the stage may be refilled
+    const uint32_t slot = consumed % kStages;
     ++consumed;
-    issue();
+    issue(slot);
   }
 };
 
@@ -346,26 +356,21 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
 
   StreamLoader<F> sl;
   if (kStream) {
-    sl.ring_s = smem_u32(smem + w * (kStages * kBatchBytes));
-    sl.bar_s = smem_u32(smem + kWarps * kStages * kBatchBytes) + w * kStages * 8;
-    sl.stash_s = smem_u32(smem + kWarps * kStages * kBatchBytes + 1024) + w * kStashBytes<F>;
-    sl.xs_s = smem_u32(smem + kWarps * kStages * kBatchBytes + 1024 + kWarps * kStashBytes<F>) +
-              w * kGroupXsBytes<F>;
+    using L = WarpSmem<F>;
+    sl.my_s = smem_u32(smem) + w * L::kBytes;
     if (lane == 0) {
-      for (int st = 0; st < kStages; ++st) mbar_init(sl.bar_s + st * 8, 1);
+      for (int st = 0; st < kStages; ++st) mbar_init(sl.my_s + L::kBars + st * 8, 1);
       fence_mbar_init();
     }
     __syncwarp();
-    sl.consumed = sl.issued = 0;
+    sl.consumed = 0;
     sl.group_batches = G * (Cfg<F>::J / kBatch);
     sl.p_left = sl.group_batches;
-    sl.p_grp = gw;
-    sl.n_full = n_full;
-    sl.W = W;
+    // groups gw, gw + W, ... below n_full: this warp streams 1 + groups_left of them
+    sl.groups_left = gw < n_full ? (int)((n_full - 1 - gw) / W) : -1;
     sl.p_ptr = reinterpret_cast<const char*>(job.x + gw * G * (int64_t)kTile);
     sl.skip_bytes = (W - 1) * G * (int64_t)kTile * (int64_t)sizeof(F);
-    sl.policy = policy_evict_first();
-    for (int st = 0; st < kStages; ++st) sl.issue();
+    for (int st = 0; st < kStages; ++st) sl.issue(st);
   }
 
   PipeLoader<F, NT> pl;
@@ -406,12 +411,12 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
       // recomputes the group with the exact path below.
       NodeFast node;
       for (int k = 0; k < G; ++k) {  // rolled
-        const F c = warp_tile_lanes<F>(sl, node, sl.stash_s);
-        st_shared(sl.xs_s + (k * 32 + lane) * (uint32_t)sizeof(F), c);
+        const F c = warp_tile_lanes<F>(sl, node, sl.my_s + WarpSmem<F>::kStash);
+        st_shared(sl.my_s + WarpSmem<F>::kXs + (k * 32 + lane) * (uint32_t)sizeof(F), c);
       }
       __syncwarp();
       if (!__any_sync(0xffffffffu, node.bad))
-        group_done = group_cross<F>(node, sl.xs_s, G, job.top_cr, gv[0],
+        group_done = group_cross<F>(node, sl.my_s + WarpSmem<F>::kXs, G, job.top_cr, gv[0],
                                     job.tile_out != nullptr ? job.tile_out + grp * G : nullptr);
       if (!group_done) {
         for (int k = 0; k < G; ++k) {  // rolled
@@ -597,21 +602,20 @@ static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
 #define NRMF_NT 1             // tiles reduced in lockstep per warp when warp groups allow it
 #endif
 
-// [ring: kWarps x kStages x 4 KiB][barriers: 1 KiB][stash: kWarps x kStashBytes]
-// [xs: kWarps x 8 tiles x 32 thread values]
-template <typename F, bool TMA>
+// Dynamic shared memory: stream kernel kWarps x WarpSmem; column (PipeLoader)
+// kernel [ring: kWarps x kStages x 4 KiB][barriers].
+template <typename F, bool TMA, bool STREAM = false>
 static size_t kernel_smem() {
-  static_assert(kWarps * kStages * 8 <= 1024, "barrier area");
-  return (TMA && NRMF_USE_TMA) ? (size_t)kWarps * kStages * kBatchBytes + 1024 +
-                                     (size_t)kWarps * (kStashBytes<F> + kGroupXsBytes<F>)
-                               : 0;
+  if (!(TMA && NRMF_USE_TMA)) return 0;
+  if (STREAM) return (size_t)kWarps * WarpSmem<F>::kBytes;
+  return (size_t)kWarps * kStages * kBatchBytes + (size_t)kWarps * kStages * 8;
 }
 
 template <typename F, bool TMA, int NT, bool STREAM>
 static int blocks_per_sm() {
   static int cached = 0;
   if (cached == 0) {
-    const size_t sm = kernel_smem<F, TMA>();
+    const size_t sm = kernel_smem<F, TMA, STREAM>();
     if (sm > 48 * 1024)
       cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sm);
@@ -696,7 +700,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   job.cta_minor = n_groups < grid * kWarps;
   grid = std::min<int64_t>(grid, n_groups);
   if (stream) {
-    nrmf_tree_kernel<F, true, 1, true><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
+    nrmf_tree_kernel<F, true, 1, true><<<(unsigned)grid, kThreads, kernel_smem<F, true, true>(), s>>>(job);
   } else if (vec && pl.g0 >= 1 && NRMF_NT == 2) {
     blocks_per_sm<F, true, NRMF_NT, false>();
     nrmf_tree_kernel<F, true, NRMF_NT, false><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
