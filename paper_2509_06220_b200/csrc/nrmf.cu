@@ -473,6 +473,92 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   if (pend_idx >= 0) climb(job, 0, pend_idx, pend_old);
 }
 
+// Small calls (few tiles): one CTA per warp group of G tiles, and the NIT
+// batches of each tile (8 rows = depth-3 subtrees of every lane) on NIT
+// different warps, so a tile costs the latency of one batch plus the levels
+// above it instead of NIT sequential batches on one warp.  The batch values
+// meet in a shared-memory stash; warp 0 evaluates the levels above the
+// batches (lanes_from_batches), the cross-thread and group levels
+// (group_cross), announces the group and climbs -- the same tree as the
+// persistent kernel.  A flagged leaf, a NaN or a partial tile: warp 0
+// recomputes the group with the exact path.
+constexpr int kSplitWarps = 8;
+template <typename F, int MODE>
+__global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const TreeJob<F> job) {
+  constexpr int V = Cfg<F>::V, NIT = Cfg<F>::J / kBatch;
+  static_assert(kSplitWarps % NIT == 0, "whole tiles per CTA");
+  __shared__ __align__(16) unsigned char stash[kSplitWarps * 32 * 16];  // [tile k][batch it][thread]
+  __shared__ __align__(16) F xs[kSplitWarps / NIT * 32];
+  __shared__ int s_bad;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = 1 << job.g0;
+  const int64_t grp = blockIdx.x;
+  const int k = w / NIT, it = w % NIT;
+  // are all G tiles of the group full tiles with data?
+  bool full = (grp + 1) * G <= job.n_items;
+  for (int t = 0; t < G && full; ++t) {
+    const F* tb;
+    int64_t remv;
+    full = tile_at(job, grp * G + t, tb, remv);
+  }
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  if (full && k < G) {
+    NodeFast node;
+    GlobalLoader<F, MODE> ld;
+    int64_t remv;
+    const F* tb;
+    tile_at(job, grp * G + k, tb, remv);
+    ld.tb = tb;
+    ld.valid = kTile;
+    ld.begin(it);
+    F r[V];
+    batch_lanes<F>(ld, node, r);
+    st_stash(smem_u32(stash) + ((k * NIT + it) * 32 + lane) * 16, r);
+    if (__any_sync(0xffffffffu, node.bad) && lane == 0) s_bad = 1;
+  }
+  __syncthreads();
+  if (w != 0) return;
+  F gv = F(0);
+  bool done = false;
+  if (full && s_bad == 0) {
+    NodeFast node;
+    for (int t = 0; t < G; ++t) {
+      F u[NIT][V];
+#pragma unroll
+      for (int i = 0; i < NIT; ++i) ld_stash(smem_u32(stash) + ((t * NIT + i) * 32 + lane) * 16, u[i]);
+      st_shared(smem_u32(xs) + (t * 32 + lane) * (uint32_t)sizeof(F), lanes_from_batches<F>(u, node));
+    }
+    __syncwarp();
+    done = group_cross<F>(node, smem_u32(xs), G, job.top_cr, gv,
+                          job.tile_out != nullptr ? job.tile_out + grp * G : nullptr);
+  }
+  if (!done) {
+    F s0[1], s1[1], s2[1], g[1];
+    NodeTop ne{job.top_cr};
+    for (int t = 0; t < G; ++t) {
+      const int64_t tau = grp * G + t;
+      g[0] = single_tile<F, MODE == kVec>(job, tau);
+      if (job.tile_out != nullptr && lane == 0 && tau < job.n_items) job.tile_out[tau] = g[0];
+      if (G == 8) counter_merge<F, 1, 8>(t, g, s0, s1, s2, ne);
+      else if (G == 4) counter_merge<F, 1, 4>(t, g, s0, s1, s2, ne);
+      else if (G == 2) counter_merge<F, 1, 2>(t, g, s0, s1, s2, ne);
+    }
+    gv = g[0];
+  }
+  if (!job.combine) return;
+  if (job.nsteps == 0) {
+    if (lane == 0) *job.out = gv;
+    return;
+  }
+  unsigned old = 0;
+  if (lane == 0) {
+    job.vals[job.val_off[0] + grp] = gv;
+    old = atom_add_release(job.cnt + job.cnt_off[0] + (grp >> job.lg_fan[0]), 1u);
+  }
+  climb(job, 0, grp, old);
+}
+
 // Balanced tree over vals[0..P) (entries >= nvals are +0) -> *out.  One CTA.
 template <typename F>
 __global__ void __launch_bounds__(kAuxThreads) bal_kernel(const F* vals, int64_t nvals, int64_t P,
@@ -598,6 +684,33 @@ static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
   return align_up((size_t)pl.n_cnt * 4, 256) + align_up((size_t)pl.n_vals * esz, 256) + 256;
 }
 
+template <typename F>
+static TreeJob<F> make_job(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int64_t len, F* tile_out,
+                           F* out, int combine, int top_cr, void* ws, size_t cnt_bytes, const Plan& pl) {
+  TreeJob<F> job;
+  job.x = x;
+  job.n_items = n_items;
+  job.tpc = tpc;
+  job.ld = ld;
+  job.len = len;
+  job.tile_out = tile_out;
+  job.cnt = reinterpret_cast<unsigned*>(ws);
+  job.vals = reinterpret_cast<F*>(static_cast<char*>(ws) + cnt_bytes);
+  job.out = out;
+  job.combine = combine;
+  job.top_cr = top_cr;
+  job.g0 = pl.g0;
+  job.cta_minor = 0;
+  job.nsteps = pl.nsteps;
+  for (int k = 0; k < kMaxSteps; ++k) {
+    job.lg_fan[k] = pl.lg_fan[k];
+    job.nin[k] = pl.nin[k];
+    job.val_off[k] = pl.val_off[k];
+    job.cnt_off[k] = pl.cnt_off[k];
+  }
+  return job;
+}
+
 #ifndef NRMF_NT
 #define NRMF_NT 1             // tiles reduced in lockstep per warp when warp groups allow it
 #endif
@@ -645,6 +758,27 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
                                                  : blocks_per_sm<F, false, 1, false>());
   if (g_grid_override > 0) grid = g_grid_override;
   // warp groups of up to 8 tiles while there is enough work for every warp
+  // Small calls: the split kernel (one CTA per group of G tiles, one warp per
+  // batch) while it needs at most two waves of CTAs.
+  {
+    constexpr int NIT = Cfg<F>::J / kBatch;
+    int g0s = 0;
+    while ((int64_t(1) << (g0s + 1)) * NIT <= kSplitWarps && (int64_t(1) << (g0s + 1)) <= p2 && combine) ++g0s;
+    if (!combine) g0s = 0;
+    const int64_t n_groups = (n_items + (int64_t(1) << g0s) - 1) >> g0s;
+    if (g_grid_override == 0 && n_groups <= 4 * (int64_t)device_sms()) {
+      const Plan pl = combine ? make_plan(n_items, p2, g0s) : make_plan(n_items, int64_t(1) << g0s, g0s);
+      const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
+      const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
+      if (combine && ws_bytes < need) return NRMF_EWORKSPACE;
+      if (combine && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
+        return NRMF_ECUDA;
+      TreeJob<F> job = make_job(x, n_items, tpc, ld, len, tile_out, out, combine, top_cr, ws, cnt_bytes, pl);
+      if (vec) nrmf_split_kernel<F, kVec><<<(unsigned)n_groups, kSplitWarps * 32, 0, s>>>(job);
+      else nrmf_split_kernel<F, kScalar><<<(unsigned)n_groups, kSplitWarps * 32, 0, s>>>(job);
+      return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
+    }
+  }
   // Warp-group size 2^g0 (<= 8 tiles).  The persistent warps take groups
   // round-robin, so the makespan is ceil(groups / W) groups of G tiles, and a
   // group costs about G + 1/3 tiles (its cross-thread tail, announce and
@@ -676,26 +810,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   // workspace across calls of different shapes or functions safe)
   if (combine && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
     return NRMF_ECUDA;
-  TreeJob<F> job;
-  job.x = x;
-  job.n_items = n_items;
-  job.tpc = tpc;
-  job.ld = ld;
-  job.len = len;
-  job.tile_out = tile_out;
-  job.cnt = reinterpret_cast<unsigned*>(ws);
-  job.vals = reinterpret_cast<F*>(static_cast<char*>(ws) + cnt_bytes);
-  job.out = out;
-  job.combine = combine;
-  job.top_cr = top_cr;
-  job.g0 = pl.g0;
-  job.nsteps = pl.nsteps;
-  for (int k = 0; k < kMaxSteps; ++k) {
-    job.lg_fan[k] = pl.lg_fan[k];
-    job.nin[k] = pl.nin[k];
-    job.val_off[k] = pl.val_off[k];
-    job.cnt_off[k] = pl.cnt_off[k];
-  }
+  TreeJob<F> job = make_job(x, n_items, tpc, ld, len, tile_out, out, combine, top_cr, ws, cnt_bytes, pl);
   const int64_t n_groups = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
   job.cta_minor = n_groups < grid * kWarps;
   grid = std::min<int64_t>(grid, n_groups);

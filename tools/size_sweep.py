@@ -1,4 +1,7 @@
-"""Dev tool: time nrmf_d / nrmf_s (device-resident input) over sizes."""
+"""Dev tool: device time of nrmf_d / nrmf_s over sizes.
+
+Each measurement replays a CUDA graph of R back-to-back calls (R = 20 for
+small n), so host overhead (Python, ctypes, launch) is not in the number."""
 import statistics
 import sys
 
@@ -8,21 +11,27 @@ sys.path.insert(0, ".")
 import paper_2509_06220_b200 as nrmf  # noqa: E402
 
 
-def t(x, reps=50):
+def t(x, reps):
     out = torch.empty((), dtype=x.dtype, device="cuda")
-    for _ in range(5):
-        nrmf.norm(x, out=out)
+    R = 20 if x.numel() <= (1 << 24) else 1
+
+    def calls():
+        for _ in range(R):
+            nrmf.norm(x, out=out)
+    g = nrmf.capture(calls)
+    for _ in range(3):
+        g.replay()
     ts = []
     for _ in range(reps):
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(); nrmf.norm(x, out=out); e1.record(); torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
+        e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / R)
     return statistics.median(ts)
 
 
 for dt in (torch.float64, torch.float32):
     for lg in (12, 16, 18, 20, 22, 24, 26, 28, 30):
         x = torch.randn(1 << lg, dtype=dt, device="cuda")
-        ms = t(x, 20 if lg >= 28 else 100)
+        ms = t(x, 20 if lg >= 28 else 50)
         print(f"{str(dt):14s} n=2^{lg:2d}: {ms*1e3:9.1f} us  {x.numel()*x.element_size()/ms/1e6:8.1f} GB/s", flush=True)
         del x
