@@ -333,6 +333,9 @@ __device__ __forceinline__ F single_tile(const TreeJob<F>& job, int64_t tau) {
   const F* tb;
   int64_t remv;
   if (tile_at(job, tau, tb, remv)) return VEC ? warp_tile<F, kVec>(tb) : warp_tile<F, kScalar>(tb);
+  bool bad = false;
+  const F v = warp_tile_padded<F>(tb, (int)remv, bad);
+  if (!bad && v == v) return v;
   return warp_tile_exact<F, kPred>(tb, (int)remv);
 }
 

@@ -310,3 +310,48 @@ def test_max_size_beyond_2p31_elements(nrmf):
     r = gpu_norm(nrmf, x)
     assert bits(r, np.float32) == bits(oracle.nrmf(x), np.float32)
     torch.cuda.empty_cache()
+
+
+PARTIAL = [1, 2, 3, 63, 64, 65, 127, 128, 129, 255, 1000, 2047, 2049, 4031, 4095]
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("valid", PARTIAL)
+def test_partial_tile_padded_fast_path(nrmf, dt, valid):
+    """Partial last tile (valid < T): the padded fast path (padding forced to
+    +0 subtree by subtree) is bit-exact with the oracle -- as the last tile of
+    a vector, and as every column of a ragged column set (rows = valid)."""
+    n = 3 * T + valid
+    x = gen.normal(valid, n, dtype=dt)
+    assert bits(gpu_norm(nrmf, x), dt) == bits(oracle.nrmf(x), dt)
+    c = 6
+    A = gen.sme(valid + 1, valid * c, dtype=dt)
+    col, fr = nrmf.cols(dev(A).as_strided((valid, c), (1, valid)))
+    ecol, efr = oracle.cols(A, valid, c, valid)
+    assert col.cpu().numpy().tobytes() == ecol.tobytes()
+    assert bits(fr.cpu().numpy(), dt) == bits(efr, dt)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("special", ["nan", "inf", "zero", "subnormal", "huge"])
+@pytest.mark.parametrize("where", ["mixed_pair", "full_pair", "first"])
+def test_partial_tile_specials(nrmf, dt, special, where):
+    """Specials inside a partial tile send it to the exact path, which keeps
+    Listing 2's semantics (e.g. v1(NaN, +0) = +0 next to padding)."""
+    valid = 700                      # lanes 0..699 valid; rows 0..ceil((700-l)/p)-1
+    n = 2 * T + valid
+    x = gen.normal(3, n, dtype=dt)
+    fi = np.finfo(dt)
+    val = {"nan": np.nan, "inf": np.inf, "zero": 0.0, "subnormal": fi.tiny / 4, "huge": fi.max / 4}[special]
+    p = 64 if dt == np.float64 else 128
+    # element of the partial tile: row j of lane l is index 2T + j*p + l
+    if where == "mixed_pair":        # lane 699's last valid row is paired with padding
+        rows = (valid - 699 + p - 1) // p
+        idx = 2 * T + (rows - 1) * p + 699
+    elif where == "full_pair":
+        idx = 2 * T + 0 * p + 5
+    else:
+        idx = 2 * T
+    x[idx] = val
+    r = gpu_norm(nrmf, x)
+    assert bits(r, dt) == bits(oracle.nrmf(x), dt)
