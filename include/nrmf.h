@@ -162,6 +162,30 @@ int nrmf_dist_ex_d(int64_t n_global, int64_t offset, int64_t count, const double
 int nrmf_dist_ex_s(int64_t n_global, int64_t offset, int64_t count, const float *x_local,
                    float *out, int flags, void *ws, size_t ws_bytes, void *nccl_comm, void *stream);
 
+/* ------------------------------------------------------------------------ */
+/* Column norms of a column-major rows x cols_global matrix whose columns are */
+/* sharded in blocks over the ranks.  Canonical block: P2c = pow2 */
+/* >= cols_global column leaves of the Frobenius tree; if world <= P2c rank r */
+/* owns columns [r*P2c/world, (r+1)*P2c/world), else rank r < P2c owns column */
+/* r; clipped to cols_global (nrmf_cols_dist_shard).  A_local holds the       */
+/* rank's col_count columns (leading dimension ld >= rows), col_norms_local    */
+/* receives their norms (bitwise those of nrmf_cols_[ds] on the whole matrix: */
+/* a column never spans ranks).  frob (device, 1 element, nullable on every   */
+/* rank or on none): the rank's block is an aligned subtree of the Frobenius  */
+/* tree (size P2c/world), one ncclAllGather of one scalar per rank follows,   */
+/* and every rank evaluates the top levels, so *frob is bitwise identical on  */
+/* every rank and equal to nrmf_cols_[ds]'s frob on one GPU.  Collective when */
+/* frob is non-null.  flags: 0 or NRMF_TOP_CR.  world a power of two.         */
+/* ------------------------------------------------------------------------ */
+int nrmf_cols_dist_shard(int64_t cols_global, int world, int rank, int64_t *col_offset, int64_t *col_count);
+size_t nrmf_cols_dist_workspace_bytes(int64_t rows, int64_t cols_global, int world, int elem_bytes);
+int nrmf_cols_dist_d(int64_t rows, int64_t cols_global, int64_t ld, int64_t col_offset, int64_t col_count,
+                     const double *A_local, double *col_norms_local, double *frob, int flags, void *ws,
+                     size_t ws_bytes, void *nccl_comm, void *stream);
+int nrmf_cols_dist_s(int64_t rows, int64_t cols_global, int64_t ld, int64_t col_offset, int64_t col_count,
+                     const float *A_local, float *col_norms_local, float *frob, int flags, void *ws,
+                     size_t ws_bytes, void *nccl_comm, void *stream);
+
 /* NCCL bootstrap helpers (libnccl.so.2 is loaded at first use; the process's
  * already-loaded NCCL, e.g. torch's, is reused).  id is 128 bytes: create it
  * on one rank, broadcast it (e.g. through torch.distributed), then call

@@ -240,6 +240,28 @@ def shard_ranges(n: int, G: int, T: int = 4096):
     return out
 
 
+def cols_shard_ranges(c: int, G: int):
+    """Canonical column blocks (DESIGN.md §9): P2c = pow2 >= c column leaves;
+    if G <= P2c rank g owns columns [g*P2c/G, (g+1)*P2c/G), else rank g < P2c
+    owns column g.  Returns [(col_offset, col_count, p2_local)] per rank."""
+    return shard_ranges(c, G, 1)
+
+
+def cols_shard_frobs(A, r: int, c: int, ld: int, G: int, top: str = "v1"):
+    """Each rank's Frobenius subtree (R_H over its column norms padded with +0
+    to p2_local), in rank order (None for a rank owning no part of the tree)."""
+    col, _ = cols(A, r, c, ld, top=top)
+    res = []
+    for (a, cnt, p2l) in cols_shard_ranges(c, G):
+        if p2l == 0:
+            res.append(None)
+            continue
+        pad = np.zeros(p2l, dtype=col.dtype)
+        pad[:cnt] = col[a:a + cnt]
+        res.append(combine(pad, top=top))
+    return res
+
+
 def shard_norms(x, G: int, top: str = "v1"):
     """Value of each rank's aligned subtree (oracle), in rank order."""
     x = _arr(x)

@@ -70,6 +70,13 @@ def _load():
             getattr(L, f).restype = i32
         L.nrmf_dist_shard.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.nrmf_dist_shard.restype = i32
+        L.nrmf_cols_dist_shard.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.nrmf_cols_dist_shard.restype = i32
+        L.nrmf_cols_dist_workspace_bytes.argtypes = [i64, i64, i32, i32]
+        L.nrmf_cols_dist_workspace_bytes.restype = sz
+        for f in ("nrmf_cols_dist_d", "nrmf_cols_dist_s"):
+            getattr(L, f).argtypes = [i64, i64, i64, i64, i64, vp, vp, vp, i32, vp, sz, vp, vp]
+            getattr(L, f).restype = i32
         L.nrmf_nccl_unique_id.argtypes = [ctypes.c_char_p]; L.nrmf_nccl_unique_id.restype = i32
         L.nrmf_nccl_comm_init.argtypes = [i32, i32, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.nrmf_nccl_comm_init.restype = i32
@@ -296,6 +303,46 @@ def dist(x_local: torch.Tensor, n_global: int, group=None, comm: Comm | None = N
         _check(f(n_global, off, cnt, x_local.data_ptr() if cnt else None, out.data_ptr(), fl, ws.data_ptr(),
                  ws.numel(), comm.handle, s.cuda_stream), "nrmf.dist")
     return out
+
+
+def cols_shard(cols_global: int, world: int, rank: int) -> tuple[int, int]:
+    """Canonical column block (col_offset, col_count) of `rank` (nrmf_cols_dist_shard)."""
+    off, cnt = ctypes.c_int64(), ctypes.c_int64()
+    _check(_load().nrmf_cols_dist_shard(cols_global, world, rank, ctypes.byref(off), ctypes.byref(cnt)),
+           "nrmf.cols_shard")
+    return off.value, cnt.value
+
+
+def cols_dist(A_local: torch.Tensor, cols_global: int, group=None, comm: Comm | None = None,
+              frob: bool = True, top: str = "v1"):
+    """Column norms of this rank's canonical column block (A_local: rows x
+    col_count, column-major, see cols_shard) and -- collectively, when frob --
+    the Frobenius norm of the whole sharded matrix, the same bits on every rank
+    and as cols() on one GPU."""
+    if A_local.dim() != 2 or not A_local.is_cuda:
+        raise ValueError("nrmf.cols_dist: 2-D CUDA tensor expected")
+    r, c = A_local.shape
+    if r > 1 and c > 0 and A_local.stride(0) != 1:
+        raise ValueError("nrmf.cols_dist: column-major storage expected (stride(0) == 1)")
+    ld = A_local.stride(1) if c > 1 else max(r, 1)
+    esz, ch = _elem(A_local.dtype)
+    fl = _flags(top)
+    comm = comm or comm_for(group)
+    off, cnt = cols_shard(cols_global, comm.world, comm.rank)
+    if c != cnt:
+        raise ValueError(f"nrmf.cols_dist: rank {comm.rank} expects {cnt} columns, got {c}")
+    L = _load()
+    dev = A_local.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream(dev)
+        col = torch.empty(c, dtype=A_local.dtype, device=dev)
+        fr = torch.empty((), dtype=A_local.dtype, device=dev) if frob else None
+        ws = _workspace(L.nrmf_cols_dist_workspace_bytes(r, cols_global, comm.world, esz), dev, s, "colsdist")
+        f = L.nrmf_cols_dist_d if ch == "d" else L.nrmf_cols_dist_s
+        _check(f(r, cols_global, ld, off, cnt, A_local.data_ptr() if A_local.numel() else None,
+                 col.data_ptr() if c else None, fr.data_ptr() if fr is not None else None, fl, ws.data_ptr(),
+                 ws.numel(), comm.handle, s.cuda_stream), "nrmf.cols_dist")
+    return (col, fr) if frob else col
 
 
 def capture(fn, warmup: int = 1) -> "torch.cuda.CUDAGraph":

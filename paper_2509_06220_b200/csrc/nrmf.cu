@@ -875,9 +875,12 @@ static int nrmf_vec(int64_t n, const F* x, F* out, int flags, void* ws, size_t w
 // values) and combines them into frob.  rows > T: tile values into the
 // workspace, then per-column trees and the frob tree (cols_combine_kernel).
 // Workspace (rows > T): [ticket 256][tile values cols*tpc][block partials]
-static size_t cols_ws_bytes(int64_t rows, int64_t cols, size_t esz) {
+// p2cols: size of the Frobenius tree over the columns (0: pow2 >= cols; a
+// larger power of two when the columns are one rank's aligned subtree of a
+// sharded matrix, nrmf_cols_dist_[ds]).
+static size_t cols_ws_bytes(int64_t rows, int64_t cols, size_t esz, int64_t p2cols = 0) {
   const int64_t tpc = std::max<int64_t>((rows + kTile - 1) / kTile, 1);
-  const int64_t p2cols = pow2_ceil(std::max<int64_t>(cols, 1));
+  if (p2cols == 0) p2cols = pow2_ceil(std::max<int64_t>(cols, 1));
   if (tpc == 1) return tree_ws_bytes(std::max<int64_t>(cols, 1), p2cols, esz);
   const int64_t nblk = (cols + kAuxThreads - 1) / kAuxThreads;
   return 256 + align_up((size_t)(cols * tpc) * esz, 256) + align_up((size_t)std::max<int64_t>(nblk, 1) * esz, 256);
@@ -885,7 +888,7 @@ static size_t cols_ws_bytes(int64_t rows, int64_t cols, size_t esz) {
 
 template <typename F>
 static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F* col_norms,
-                          F* frob, int flags, void* ws, size_t ws_bytes, void* stream) {
+                          F* frob, int flags, void* ws, size_t ws_bytes, void* stream, int64_t p2_override = 0) {
   const int cr = flags & NRMF_TOP_CR;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (rows < 0 || cols < 0 || ld < rows || ld < 0) return NRMF_EINVAL;
@@ -903,9 +906,9 @@ static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F*
     if (frob && cudaMemsetAsync(frob, 0, sizeof(F), s) != cudaSuccess) return NRMF_ECUDA;
     return NRMF_OK;
   }
-  if (ws_bytes < cols_ws_bytes(rows, cols, sizeof(F))) return NRMF_EWORKSPACE;
+  if (ws_bytes < cols_ws_bytes(rows, cols, sizeof(F), p2_override)) return NRMF_EWORKSPACE;
   const int64_t tpc = (rows + kTile - 1) / kTile;
-  const int64_t p2cols = pow2_ceil(cols);
+  const int64_t p2cols = p2_override > 0 ? p2_override : pow2_ceil(cols);
   const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && ((ld * (int64_t)sizeof(F)) & 15) == 0;
   if (tpc == 1)
     return launch_tree<F>(A, cols, 1, ld, rows, p2cols, col_norms, frob, frob != nullptr ? 1 : 0, ws, ws_bytes,
@@ -921,6 +924,19 @@ static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F*
   cols_combine_kernel<F><<<(unsigned)nblk, kAuxThreads, 0, s>>>(vals, cols, tpc, pow2_ceil(tpc), col_norms,
                                                             p2cols, partials, ticket, frob, cr);
   return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
+}
+
+template <typename F>
+int cols_eval(int64_t rows, int64_t cols, int64_t ld, const F* A, F* col_norms, F* frob, int64_t p2cols,
+              int flags, void* ws, size_t ws_bytes, cudaStream_t s) {
+  return nrmf_cols_impl<F>(rows, cols, ld, A, col_norms, frob, flags, ws, ws_bytes, s, p2cols);
+}
+template int cols_eval<double>(int64_t, int64_t, int64_t, const double*, double*, double*, int64_t, int, void*,
+                               size_t, cudaStream_t);
+template int cols_eval<float>(int64_t, int64_t, int64_t, const float*, float*, float*, int64_t, int, void*,
+                              size_t, cudaStream_t);
+size_t cols_workspace(int64_t rows, int64_t cols, int64_t p2cols, size_t esz) {
+  return cols_ws_bytes(rows, cols, esz, p2cols);
 }
 
 // ---------------------------------------------------------------- host input

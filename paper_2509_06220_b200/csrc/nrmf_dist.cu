@@ -93,6 +93,25 @@ int64_t shard(int64_t n, int world, int rank, int64_t* off, int64_t* cnt) {
   return p2l;
 }
 
+// Canonical aligned partition of P2 = pow2 >= units leaves (tiles or columns)
+// over world ranks: [t0, t1) and the local subtree size (0 = none).
+int64_t shard_units(int64_t units, int world, int rank, int64_t* t0, int64_t* t1) {
+  const int64_t P2 = pow2_ceil(std::max<int64_t>(units, 1));
+  if (world <= P2) {
+    const int64_t per = P2 / world;
+    *t0 = rank * per;
+    *t1 = *t0 + per;
+    return per;
+  }
+  if (rank < P2) {
+    *t0 = rank;
+    *t1 = rank + 1;
+    return 1;
+  }
+  *t0 = *t1 = P2;
+  return 0;
+}
+
 // workspace: [local tree ws][local value (256)][gathered (world entries)]
 size_t dist_ws(int64_t n, int world, size_t esz) {
   const int64_t nt = (n + kTileE - 1) / kTileE;
@@ -146,6 +165,60 @@ int dist_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, void
   return bal_eval<F>(gathered, nr, nr, out, s, cr);
 }
 
+// ---------------------------------------------------------------- columns
+// Column blocks: rank r owns columns [t0, t1) of the canonical partition of
+// the P2c = pow2 >= cols column leaves of the Frobenius tree; its column norms
+// are local (each column lies on one rank), its block's Frobenius subtree
+// (size P2c/world, padded with +0) is exchanged as one scalar, and every rank
+// evaluates the top lg min(world, P2c) levels.
+// workspace: [local cols ws][local value (256)][gathered (world entries)]
+size_t cols_dist_ws(int64_t rows, int64_t cols, int world, size_t esz) {
+  int64_t t0, t1;
+  const int64_t p2l = std::max<int64_t>(shard_units(cols, world, 0, &t0, &t1), 1);
+  const int64_t cl = std::max<int64_t>(std::min(t1, cols) - std::min(t0, cols), 1);
+  return align_up(cols_workspace(rows, cl, p2l, esz), 256) + 256 + align_up((size_t)world * esz, 256);
+}
+
+template <typename F>
+int cols_dist_impl(int64_t rows, int64_t cols, int64_t ld, int64_t col_off, int64_t col_cnt, const F* A,
+                   F* col_norms, F* frob, int flags, void* ws, size_t ws_bytes, void* comm_v, void* stream) {
+  if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
+  const int cr = flags & NRMF_TOP_CR;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (rows < 0 || cols < 0 || ld < rows || col_off < 0 || col_cnt < 0) return NRMF_EINVAL;
+  if (comm_v == nullptr || ws == nullptr) return NRMF_EINVAL;
+  const NcclApi* api = nccl();
+  if (api == nullptr) return NRMF_ENCCL;
+  ncclComm_t comm = static_cast<ncclComm_t>(comm_v);
+  int world = 0, rank = 0;
+  if (api->CommCount(comm, &world) != ncclSuccess || api->CommUserRank(comm, &rank) != ncclSuccess)
+    return NRMF_ENCCL;
+  if (!is_pow2(world)) return NRMF_ESHARD;
+  int64_t t0, t1;
+  const int64_t p2l = shard_units(cols, world, rank, &t0, &t1);
+  const int64_t a = std::min(t0, cols), b = std::min(t1, cols);
+  if (col_off != a || col_cnt != b - a) return NRMF_ESHARD;
+  if (ws_bytes < cols_dist_ws(rows, cols, world, sizeof(F))) return NRMF_EWORKSPACE;
+  char* p = static_cast<char*>(ws);
+  const size_t lws = align_up(cols_workspace(rows, std::max<int64_t>(col_cnt, 1), std::max<int64_t>(p2l, 1),
+                                             sizeof(F)), 256);
+  F* local = reinterpret_cast<F*>(p + lws);
+  F* gathered = reinterpret_cast<F*>(p + lws + 256);
+  int st = NRMF_OK;
+  if (col_cnt > 0) {
+    st = cols_eval<F>(rows, col_cnt, ld, A, col_norms, frob != nullptr ? local : nullptr, p2l, flags, ws, lws, s);
+  } else if (frob != nullptr && cudaMemsetAsync(local, 0, sizeof(F), s) != cudaSuccess) {
+    st = NRMF_ECUDA;  // no columns here: an all-padding subtree (value +0)
+  }
+  if (st != NRMF_OK || frob == nullptr) return st;
+  if (reinterpret_cast<uintptr_t>(frob) % sizeof(F)) return NRMF_EALIGN;
+  const ncclDataType_t dt = sizeof(F) == 8 ? ncclFloat64 : ncclFloat32;
+  if (api->AllGather(local, gathered, 1, dt, comm, s) != ncclSuccess) return NRMF_ENCCL;
+  const int64_t P2c = pow2_ceil(std::max<int64_t>(cols, 1));
+  const int64_t nr = std::min<int64_t>(world, P2c);
+  return bal_eval<F>(gathered, nr, nr, frob, s, cr);
+}
+
 }  // namespace
 }  // namespace nrmf
 
@@ -180,6 +253,34 @@ int nrmf_dist_ex_d(int64_t n_global, int64_t offset, int64_t count, const double
 int nrmf_dist_ex_s(int64_t n_global, int64_t offset, int64_t count, const float* x_local, float* out,
                    int flags, void* ws, size_t ws_bytes, void* nccl_comm, void* stream) {
   return dist_impl<float>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream, flags);
+}
+
+int nrmf_cols_dist_shard(int64_t cols_global, int world, int rank, int64_t* col_offset, int64_t* col_count) {
+  if (cols_global < 0 || world < 1 || rank < 0 || rank >= world || !col_offset || !col_count) return NRMF_EINVAL;
+  if (!is_pow2(world)) return NRMF_ESHARD;
+  int64_t t0, t1;
+  shard_units(cols_global, world, rank, &t0, &t1);
+  *col_offset = std::min(t0, cols_global);
+  *col_count = std::min(t1, cols_global) - *col_offset;
+  return NRMF_OK;
+}
+
+size_t nrmf_cols_dist_workspace_bytes(int64_t rows, int64_t cols_global, int world, int elem_bytes) {
+  if (rows < 0 || cols_global < 0 || world < 1 || (elem_bytes != 4 && elem_bytes != 8)) return 0;
+  return cols_dist_ws(rows, cols_global, world, (size_t)elem_bytes);
+}
+
+int nrmf_cols_dist_d(int64_t rows, int64_t cols_global, int64_t ld, int64_t col_offset, int64_t col_count,
+                     const double* A_local, double* col_norms_local, double* frob, int flags, void* ws,
+                     size_t ws_bytes, void* nccl_comm, void* stream) {
+  return cols_dist_impl<double>(rows, cols_global, ld, col_offset, col_count, A_local, col_norms_local, frob,
+                                flags, ws, ws_bytes, nccl_comm, stream);
+}
+int nrmf_cols_dist_s(int64_t rows, int64_t cols_global, int64_t ld, int64_t col_offset, int64_t col_count,
+                     const float* A_local, float* col_norms_local, float* frob, int flags, void* ws,
+                     size_t ws_bytes, void* nccl_comm, void* stream) {
+  return cols_dist_impl<float>(rows, cols_global, ld, col_offset, col_count, A_local, col_norms_local, frob,
+                               flags, ws, ws_bytes, nccl_comm, stream);
 }
 
 int nrmf_nccl_unique_id(char* id128) {

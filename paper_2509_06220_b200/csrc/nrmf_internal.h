@@ -15,4 +15,10 @@ template <typename F>
 int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s, int top_cr);
 // Workspace bytes of tree_eval for a p2-tile tree.
 size_t tree_workspace(int64_t p2, size_t esz);
+// Column norms + Frobenius tree of size p2cols (a power of two >= cols) over
+// them; arguments validated like nrmf_cols_ex_[ds].
+template <typename F>
+int cols_eval(int64_t rows, int64_t cols, int64_t ld, const F* A, F* col_norms, F* frob, int64_t p2cols,
+              int flags, void* ws, size_t ws_bytes, cudaStream_t s);
+size_t cols_workspace(int64_t rows, int64_t cols, int64_t p2cols, size_t esz);
 }  // namespace nrmf

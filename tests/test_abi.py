@@ -94,3 +94,14 @@ def test_shard_rejects_non_power_of_two(L):
     import paper_2509_06220_b200 as nrmf
     with pytest.raises(RuntimeError):
         nrmf.shard(1000, 3, 0)
+
+
+@pytest.mark.parametrize("c,G", [(65536, 1), (65536, 8), (5, 8), (7, 4), (1, 2), (0, 4), (100, 2)])
+def test_cols_shard_partition_matches_oracle_reading(c, G):
+    """nrmf_cols_dist_shard (C, host-only) == the oracle's restatement of the
+    canonical column blocks; blocks cover [0, c) contiguously."""
+    import paper_2509_06220_b200 as nrmf
+    exp = oracle.cols_shard_ranges(c, G)
+    got = [nrmf.cols_shard(c, G, g) for g in range(G)]
+    assert got == [(a, n) for a, n, _ in exp]
+    assert sum(n for _, n in got) == c

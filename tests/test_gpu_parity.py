@@ -355,3 +355,31 @@ def test_partial_tile_specials(nrmf, dt, special, where):
     x[idx] = val
     r = gpu_norm(nrmf, x)
     assert bits(r, dt) == bits(oracle.nrmf(x), dt)
+
+
+def test_cols_dist_world1(nrmf):
+    """nrmf_cols_dist_[ds] on a 1-rank NCCL communicator: column norms and the
+    Frobenius norm equal nrmf_cols bitwise (and the oracle)."""
+    import torch.distributed as td
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29537")
+    created = False
+    if not td.is_initialized():
+        td.init_process_group("gloo", rank=0, world_size=1)
+        created = True
+    try:
+        for dt in (np.float64, np.float32):
+            for (r, c) in ((4096, 33), (5000, 7), (100, 65)):
+                A = gen.normal(r + c, r * c, dtype=dt)
+                At = dev(A).as_strided((r, c), (1, r))
+                col, fr = nrmf.cols_dist(At, c)
+                ecol, efr = oracle.cols(A, r, c, r)
+                assert col.cpu().numpy().tobytes() == ecol.tobytes()
+                assert bits(fr.cpu().numpy(), dt) == bits(efr, dt)
+                assert nrmf.cols_dist(At, c, frob=False).cpu().numpy().tobytes() == ecol.tobytes()
+    finally:
+        for cm in list(nrmf._comms.values()):
+            cm.close()
+        nrmf._comms.clear()
+        if created:
+            td.destroy_process_group()

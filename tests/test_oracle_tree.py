@@ -277,3 +277,22 @@ def test_A_top_reading_R1_f1():
     eps = mpmath.mpf(2) ** -53
     ub = float(((oracle.reH_plus()) ** 12 * (1 + eps) ** 6 - 1) / eps)   # 12 v1 levels, 6 cr levels
     assert oracle.relerr(a, oracle.exact(z)) <= ub
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("r,c", [(5, 7), (4096, 9), (4100, 3), (1, 33), (300, 64)])
+def test_cols_block_shards_combine_to_global_frob(dt, r, c):
+    """Column blocks: each rank's Frobenius subtree over its
+    canonical column block, padded to P2c/G, combined by the rank tree, equals
+    the global Frobenius norm bitwise for every G = 1..8 (powers of two) --
+    including a NaN column norm, for which +0 padding is not neutral (R4)."""
+    A = gen.normal(r * 10 + c, r * c, dtype=dt)
+    for with_nan in (False, True):
+        if with_nan:
+            A = A.copy()
+            A[(c - 1) * r:] = np.nan           # last column all NaN: its norm is NaN
+        _, efr = oracle.cols(A, r, c, r)
+        for G in (1, 2, 4, 8):
+            vals = oracle.cols_shard_frobs(A, r, c, r, G)
+            got = oracle.combine_ranks(vals)
+            assert np.asarray(got, dtype=dt).tobytes() == np.asarray(efr, dtype=dt).tobytes(), (G, with_nan)
