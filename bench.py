@@ -386,6 +386,10 @@ def run_ours(args):
         line["context_sumsq"] = sumsq_context(x, ex, dt, ms, args, stream)
         if config == "c3" and not args.no_snrmf:
             line["snrmf"] = snrmf_point(nrmf, device, stream, args, hbm_peak)
+        if config == "c3" and not args.no_other:
+            del x
+            torch.cuda.empty_cache()
+            line["other_configs"] = other_configs(nrmf, device, stream, hbm_peak)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -487,6 +491,67 @@ def sumsq_context(x, ex, dt, ms_nrmf, args, stream):
             "ulp": ulp_distance(v, ex, dt)}
 
 
+def other_configs(nrmf, device, stream, hbm_peak):
+    """The other BASELINE configs, reported beside the metric (parity-test
+    cases, not bench lines): C2 SNRMF n=2^28, C4 column norms 4096 x 65536,
+    C5 extreme range n=2^27 (three readings, R9) and its complex view.  Inputs
+    device-resident, each timed as 20 graph replays after warm-up; bits checked
+    against the oracle."""
+    import torch
+
+    import nrmf_inputs as gen
+    import oracle
+
+    def timed(fn, reps=20):
+        g = nrmf.capture(fn)
+        for _ in range(3):
+            g.replay()
+        return time_loop(g.replay, reps, stream)
+
+    res = {}
+    n2 = 1 << 28
+    x2h = gen.sme(1, n2)
+    x2 = torch.from_numpy(x2h).to(device)
+    o2 = torch.empty((), dtype=torch.float32, device=device)
+    ms = timed(lambda: nrmf.norm(x2, out=o2))
+    res["C2"] = {"workload": "SNRMF fp32 n=2^28 s*m*2^e", "ms": round(ms, 4),
+                 "GB/s": round(n2 * 4 / (ms * 1e-3) / 1e9, 1), "hbm_frac": round(n2 * 4 / (ms * 1e-3) / 1e9 / hbm_peak, 4),
+                 "bit_exact_vs_oracle": bool(o2.cpu().numpy().tobytes() == np.float32(oracle.nrmf(x2h)).tobytes())}
+    del x2, x2h
+    r, c = 4096, 65536
+    Ah = gen.colscaled_normal(1, r, c)
+    A = torch.from_numpy(Ah).to(device).as_strided((r, c), (1, r))
+    col = torch.empty(c, dtype=torch.float64, device=device)
+    fr = torch.empty((), dtype=torch.float64, device=device)
+
+    def colsc():
+        cc, ff = nrmf.cols(A)
+        col.copy_(cc)
+        fr.copy_(ff)
+    ms = timed(colsc)
+    ecol, efr = oracle.cols(Ah, r, c, r)
+    res["C4"] = {"workload": "nrmf_cols_d 4096 x 65536 N(0,1)*2^k_j", "ms": round(ms, 4),
+                 "GB/s": round(r * c * 8 / (ms * 1e-3) / 1e9, 1),
+                 "hbm_frac": round(r * c * 8 / (ms * 1e-3) / 1e9 / hbm_peak, 4),
+                 "bit_exact_vs_oracle": bool(col.cpu().numpy().tobytes() == ecol.tobytes()
+                                             and fr.cpu().numpy().tobytes() == np.float64(efr).tobytes())}
+    del A, Ah
+    n5 = 1 << 27
+    for variant in ("lit", "fin", "fin2"):
+        xh = gen.extreme(1, n5, variant)
+        xd = torch.from_numpy(xh).to(device)
+        o = torch.empty((), dtype=torch.float64, device=device)
+        ms = timed(lambda: nrmf.norm(xd, out=o))
+        oz = nrmf.norm_complex(xd.view(torch.complex128)).cpu().numpy()
+        exp = np.float64(oracle.nrmf(xh))
+        res["C5_" + variant] = {"workload": f"DNRMF fp64 n=2^27 extreme range ({variant})", "ms": round(ms, 4),
+                                "GB/s": round(n5 * 8 / (ms * 1e-3) / 1e9, 1),
+                                "bit_exact_vs_oracle": bool(o.cpu().numpy().tobytes() == exp.tobytes()),
+                                "complex_view_same_bits": bool(oz.tobytes() == exp.tobytes())}
+        del xd, xh
+    return res
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -508,6 +573,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-snrmf", action="store_true")
+    ap.add_argument("--no-other", action="store_true", help="skip the C2/C4/C5 report (other_configs)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
