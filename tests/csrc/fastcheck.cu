@@ -211,6 +211,32 @@ __global__ void check_internal_s(uint64_t seed, uint64_t n, Counts* c) {
   atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
 }
 
+// fp64 division near rounding midpoints: M random in [1, 2) (scaled by a
+// random power of two in the fast domain), a midpoint c = (2K+1) 2^-54 of the
+// quotient grid in [2^-k-1, 2^-k), and m = RN(M * c) (+- a few ulps), so that
+// m/M lies within about an ulp of m of a midpoint of q -- the hardest inputs
+// for a correctly rounded division.  The fast sequence must equal __ddiv_rn.
+__global__ void check_div_d_midpoints(uint64_t seed, uint64_t n, Counts* c) {
+  unsigned long long ck = 0, mi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    const double Mb = 1.0 + (double)(k >> 12) * 0x1p-52;
+    const int kq = (int)(mix(k + 1) % 60);                     // quotient binade [2^-kq-1, 2^-kq)
+    const uint64_t K = mix(k + 2) >> 12;                        // 52-bit mantissa index
+    const double cmid = ldexp(1.0 + ((double)K + 0.5) * 0x1p-52, -kq - 1);   // midpoint of that binade
+    double m = __dmul_rn(Mb, cmid);
+    m = __longlong_as_double(__double_as_longlong(m) + (long long)((int)(mix(k + 3) % 5) - 2));
+    if (m > Mb) m = Mb;
+    const int e = (int)(mix(k + 4) % 1800) - 890;               // common scale, stays in [2^-890, 2^911)
+    const double M1[1] = {ldexp(Mb, e)}, m1[1] = {ldexp(m, e)};
+    double q[1];
+    fast_div_n<1>(m1, M1, q);
+    ++ck;
+    if (__double_as_longlong(q[0]) != __double_as_longlong(__ddiv_rn(m1[0], M1[0]))) ++mi;
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
+}
+
 extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long n, int mode,
                          unsigned long long* out3) {
   Counts* c;
@@ -224,6 +250,7 @@ extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long 
     case 4: check_sqrt_d<<<148 * 8, 256>>>(seed, n, c); break;
     case 5: check_internal_d<<<148 * 8, 256>>>(seed, n, c); break;
     case 6: check_internal_s<<<148 * 8, 256>>>(seed, n, c); break;
+    case 7: check_div_d_midpoints<<<148 * 8, 256>>>(seed, n, c); break;
     default: return 2;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return 3;

@@ -81,3 +81,12 @@ def test_internal_node_unchecked_in_fast_domain(fc, which):
     subnormal and zero m)."""
     checked, fast, mism = fc(which, seed=31 + which, n=1 << 28)
     assert checked == 1 << 28 and fast == checked and mism == 0
+
+
+def test_fp64_division_near_midpoints(fc):
+    """2^30 divisions m/M constructed to lie within about an ulp of m of a
+    rounding midpoint of the quotient (m = RN(M*c), c a midpoint, +-2 ulps),
+    over 60 quotient binades and scales across the fast domain: the fast
+    sequence equals __ddiv_rn on every one."""
+    checked, _, mism = fc(7, seed=77, n=1 << 30)
+    assert checked == 1 << 30 and mism == 0
