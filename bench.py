@@ -236,10 +236,17 @@ def run_ours(args):
     out = torch.empty((), dtype=tdt, device=device)
     comm = nrmf.comm_for(None) if world > 1 else None
 
+    p2p = world > 1 and os.environ.get("NRMF_BENCH_P2P", "0") == "1"
+    pgroup = nrmf.P2PGroup() if p2p else None
     if world > 1:
-        # one CUDA graph per step: counter memset, tile-tree kernel, ncclAllGather
-        # of one scalar, rank-tree kernel
-        graph = nrmf.capture(lambda: nrmf.dist(x, n, comm=comm, out=out))
+        # one CUDA graph per step: counter memset, tile-tree kernel, and either
+        # ncclAllGather of one scalar + rank-tree kernel, or with
+        # NRMF_BENCH_P2P=1 the peer-memory exchange kernel (opt-in:
+        # validated by emulated ranks on one GPU, not yet on several)
+        if p2p:
+            graph = nrmf.capture(lambda: nrmf.dist_p2p(x, n, pgroup, out=out))
+        else:
+            graph = nrmf.capture(lambda: nrmf.dist(x, n, comm=comm, out=out))
 
         def step():
             graph.replay()
@@ -302,6 +309,7 @@ def run_ours(args):
                    "tree_version": nrmf.tree_version(), "seed": 1},
         "gpu_launches": launches_per_step * args.steps,
         "graph": True,
+        "rank_exchange": ("p2p" if p2p else "nccl_allgather") if world > 1 else None,
         "clocks": clocks,
         "elements_per_s": round(n / (ms * 1e-3), 1),
         "roofline": {"bound": "hbm", "achieved": round(kern_gbs, 2), "peak": hbm_peak, "unit": "GB/s",
@@ -393,6 +401,8 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        if pgroup is not None:
+            pgroup.close()
         comm.close()
         td.destroy_process_group()
     return 0

@@ -186,6 +186,40 @@ int nrmf_cols_dist_s(int64_t rows, int64_t cols_global, int64_t ld, int64_t col_
                      const float *A_local, float *col_norms_local, float *frob, int flags, void *ws,
                      size_t ws_bytes, void *nccl_comm, void *stream);
 
+/* ------------------------------------------------------------------------ */
+/* The rank level through peer memory instead of NCCL: the same  */
+/* canonical shards and the same rank tree as nrmf_dist_[ds], but the rank    */
+/* values are exchanged by one warp per rank with P2P stores into every       */
+/* peer's buffer (CUDA IPC over NVLink) and a flag, then each rank evaluates   */
+/* the rank tree -- one tiny kernel instead of ncclAllGather + a kernel.       */
+/* Setup (once per rank, collective through the caller's own channel):        */
+/*   nrmf_p2p_alloc(&buf) -- nrmf_p2p_buffer_bytes() of device memory,       */
+/*     zero-filled (the one allocation the library makes; free it with     */
+/*     nrmf_p2p_free);                                                      */
+/*   nrmf_p2p_ipc_handle(buf, h) -- 64-byte CUDA IPC handle, all-gathered;    */
+/*   nrmf_p2p_open(h_r, &ptr_r) for every other rank r (close: _p2p_close);   */
+/*   peers: a DEVICE array of world pointers, peers[r] = rank r's buffer as  */
+/*     mapped in this process, peers[rank] = buf.                             */
+/* Calls: every rank makes the same sequence of calls; the buffer keeps a    */
+/* call counter and two parity halves, so nothing is reset between calls and */
+/* a call can be captured in a CUDA graph.  err (device u32, nullable) is set */
+/* to 1 if a rank's value did not arrive within ~seconds (out is then NaN     */
+/* instead of a hang).  world: a power of two <= 32.                          */
+/* Every rank's out has the same bits, equal to nrmf_[ds] on one GPU.         */
+/* ------------------------------------------------------------------------ */
+size_t nrmf_p2p_buffer_bytes(void);
+int nrmf_p2p_alloc(void **buf);
+int nrmf_p2p_free(void *buf);
+int nrmf_p2p_ipc_handle(const void *buf, char *handle64);
+int nrmf_p2p_open(const char *handle64, void **peer_buf);
+int nrmf_p2p_close(void *peer_buf);
+int nrmf_dist_p2p_d(int64_t n_global, int64_t offset, int64_t count, const double *x_local, double *out,
+                    int flags, void *ws, size_t ws_bytes, const void *peers, int world, int rank,
+                    unsigned *err, void *stream);
+int nrmf_dist_p2p_s(int64_t n_global, int64_t offset, int64_t count, const float *x_local, float *out,
+                    int flags, void *ws, size_t ws_bytes, const void *peers, int world, int rank,
+                    unsigned *err, void *stream);
+
 /* NCCL bootstrap helpers (libnccl.so.2 is loaded at first use; the process's
  * already-loaded NCCL, e.g. torch's, is reused).  id is 128 bytes: create it
  * on one rank, broadcast it (e.g. through torch.distributed), then call

@@ -70,6 +70,18 @@ def _load():
             getattr(L, f).restype = i32
         L.nrmf_dist_shard.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.nrmf_dist_shard.restype = i32
+        L.nrmf_p2p_buffer_bytes.argtypes = []; L.nrmf_p2p_buffer_bytes.restype = sz
+        L.nrmf_p2p_alloc.argtypes = [ctypes.POINTER(vp)]; L.nrmf_p2p_alloc.restype = i32
+        L.nrmf_p2p_free.argtypes = [vp]; L.nrmf_p2p_free.restype = i32
+        L.nrmf_p2p_ipc_handle.argtypes = [vp, ctypes.c_char_p]; L.nrmf_p2p_ipc_handle.restype = i32
+        L.nrmf_p2p_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]; L.nrmf_p2p_open.restype = i32
+        L.nrmf_p2p_close.argtypes = [vp]; L.nrmf_p2p_close.restype = i32
+        for f in ("nrmf_dist_p2p_d", "nrmf_dist_p2p_s"):
+            getattr(L, f).argtypes = [i64, i64, i64, vp, vp, i32, vp, sz, vp, i32, i32, vp, vp]
+            getattr(L, f).restype = i32
+        for f in ("nrmf_debug_p2p_emulate_d", "nrmf_debug_p2p_emulate_s"):
+            getattr(L, f).argtypes = [i32, vp, vp, i32, vp, vp]
+            getattr(L, f).restype = i32
         L.nrmf_cols_dist_shard.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.nrmf_cols_dist_shard.restype = i32
         L.nrmf_cols_dist_workspace_bytes.argtypes = [i64, i64, i32, i32]
@@ -303,6 +315,91 @@ def dist(x_local: torch.Tensor, n_global: int, group=None, comm: Comm | None = N
         _check(f(n_global, off, cnt, x_local.data_ptr() if cnt else None, out.data_ptr(), fl, ws.data_ptr(),
                  ws.numel(), comm.handle, s.cuda_stream), "nrmf.dist")
     return out
+
+
+class P2PGroup:
+    """Peer-memory rank exchange for dist_p2p: allocates this rank's
+    exchange buffer, all-gathers the CUDA IPC handles through the
+    torch.distributed group, maps every peer's buffer and keeps the device
+    array of peer pointers.  One per (group, device); every rank must make the
+    same sequence of dist_p2p calls on it (the call counter lives in the
+    buffer, so calls may be captured in CUDA graphs)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        L = _load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > 32:
+            raise ValueError("nrmf.P2PGroup: at most 32 ranks")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        buf = ctypes.c_void_p()
+        _check(L.nrmf_p2p_alloc(ctypes.byref(buf)), "nrmf_p2p_alloc")
+        self.buf = buf
+        h = ctypes.create_string_buffer(64)
+        _check(L.nrmf_p2p_ipc_handle(buf, h), "nrmf_p2p_ipc_handle")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h.raw), group=group)
+        self._opened = []
+        ptrs = []
+        for r in range(self.world):
+            if r == self.rank:
+                ptrs.append(buf.value)
+                continue
+            p = ctypes.c_void_p()
+            _check(L.nrmf_p2p_open(ctypes.c_char_p(handles[r]), ctypes.byref(p)), "nrmf_p2p_open")
+            self._opened.append(p)
+            ptrs.append(p.value)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        dist.barrier(group=group)   # every buffer is mapped before the first exchange
+
+    def close(self):
+        L = _load()
+        for p in self._opened:
+            L.nrmf_p2p_close(p)
+        self._opened = []
+        if self.buf:
+            L.nrmf_p2p_free(self.buf)
+            self.buf = None
+
+
+def dist_p2p(x_local: torch.Tensor, n_global: int, pg: P2PGroup, out: torch.Tensor | None = None,
+             top: str = "v1") -> torch.Tensor:
+    """As dist(), with the rank values exchanged through peer memory (one
+    kernel, no NCCL).  Collective over pg's ranks; same bits on every rank and
+    as norm() of the whole array on one GPU.  pg.err turns 1 if an exchange
+    timed out (the result is then NaN)."""
+    if not x_local.is_cuda or not x_local.is_contiguous():
+        raise ValueError("nrmf.dist_p2p: contiguous CUDA tensor expected")
+    esz, c = _elem(x_local.dtype)
+    fl = _flags(top)
+    off, cnt = shard(n_global, pg.world, pg.rank)
+    if x_local.numel() != cnt:
+        raise ValueError(f"nrmf.dist_p2p: rank {pg.rank} expects {cnt} elements, got {x_local.numel()}")
+    L = _load()
+    dev = x_local.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream(dev)
+        if out is None:
+            out = torch.empty((), dtype=x_local.dtype, device=dev)
+        ws = _workspace(L.nrmf_dist_workspace_bytes(n_global, pg.world, esz), dev, s, "dist")
+        f = L.nrmf_dist_p2p_d if c == "d" else L.nrmf_dist_p2p_s
+        _check(f(n_global, off, cnt, x_local.data_ptr() if cnt else None, out.data_ptr(), fl, ws.data_ptr(),
+                 ws.numel(), pg.peers.data_ptr(), pg.world, pg.rank, pg.err.data_ptr(),
+                 s.cuda_stream), "nrmf.dist_p2p")
+    return out
+
+
+def _debug_p2p_emulate(values: torch.Tensor, bufs: torch.Tensor, top: str = "v1") -> torch.Tensor:
+    """Test hook: len(values) ranks emulated as the CTAs of one cooperative
+    launch on this GPU (bufs: device int64 array of their zeroed buffers)."""
+    esz, c = _elem(values.dtype)
+    outs = torch.empty_like(values)
+    f = _load().nrmf_debug_p2p_emulate_d if c == "d" else _load().nrmf_debug_p2p_emulate_s
+    _check(f(values.numel(), values.data_ptr(), bufs.data_ptr(), _flags(top), outs.data_ptr(),
+             torch.cuda.current_stream().cuda_stream), "nrmf p2p emulate")
+    return outs
 
 
 def cols_shard(cols_global: int, world: int, rank: int) -> tuple[int, int]:

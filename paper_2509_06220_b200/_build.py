@@ -9,7 +9,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libnrmf.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("nrmf.cu", "nrmf_dist.cu")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("nrmf_device.cuh", "nrmf_internal.h",
-                                                           "nrmf_crhypot.cuh")] + [
+                                                           "nrmf_crhypot.cuh", "nrmf_p2p.cuh")] + [
     os.path.join(ROOT, "include", "nrmf.h")]
 
 NVCC_FLAGS = [

@@ -23,6 +23,7 @@
 
 #include "../../include/nrmf.h"
 #include "nrmf_internal.h"
+#include "nrmf_p2p.cuh"
 
 namespace nrmf {
 namespace {
@@ -165,6 +166,73 @@ int dist_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, void
   return bal_eval<F>(gathered, nr, nr, out, s, cr);
 }
 
+// ---------------------------------------------------------------- peer memory
+// The rank level through peer memory (nrmf_p2p.cuh): one warp per rank.
+template <typename F>
+__global__ void __launch_bounds__(32) p2p_exchange_kernel(const F* local, PeerArgs a, int nr, int cr, F* out) {
+  const F v = rank_exchange<F>(*local, a, nr, cr);
+  if (threadIdx.x == 0) *out = v;
+}
+
+// Test emulation of `world` ranks on one GPU as the CTAs of ONE cooperative
+// launch (co-resident by construction): CTA r plays rank r with value
+// values[r], every rank's buffer lives on this GPU.
+template <typename F>
+__global__ void __launch_bounds__(32) p2p_emulate_kernel(const F* values, PeerArgs a, int nr, int cr, F* outs) {
+  PeerArgs b = a;
+  b.rank = (int)blockIdx.x;
+  const F v = rank_exchange<F>(values[blockIdx.x], b, nr, cr);
+  if (threadIdx.x == 0) outs[blockIdx.x] = v;
+}
+
+template <typename F>
+int dist_p2p_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, int flags, void* ws,
+                  size_t ws_bytes, const void* peers, int world, int rank, unsigned* err, void* stream) {
+  if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
+  const int cr = flags & NRMF_TOP_CR;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (peers == nullptr || out == nullptr || ws == nullptr || n < 0) return NRMF_EINVAL;
+  if (world < 1 || world > kP2PMaxRanks || rank < 0 || rank >= world) return NRMF_EINVAL;
+  if (!is_pow2(world)) return NRMF_ESHARD;
+  if (count > 0 && x == nullptr) return NRMF_EINVAL;
+  if (reinterpret_cast<uintptr_t>(x) % sizeof(F) || reinterpret_cast<uintptr_t>(out) % sizeof(F))
+    return NRMF_EALIGN;
+  int64_t off = 0, cnt = 0;
+  const int64_t p2l = shard(n, world, rank, &off, &cnt);
+  if (off != offset || cnt != count) return NRMF_ESHARD;
+  if (ws_bytes < dist_ws(n, world, sizeof(F))) return NRMF_EWORKSPACE;
+  const int64_t nt = (n + kTileE - 1) / kTileE;
+  const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
+  const int64_t p2ws = world <= P2 ? P2 / world : 1;
+  char* p = static_cast<char*>(ws);
+  const size_t tws = tree_workspace(p2ws, sizeof(F));
+  F* local = reinterpret_cast<F*>(p + tws);
+  int st = NRMF_OK;
+  if (p2l > 0 && cnt > 0) {
+    st = tree_eval<F>(cnt, x, p2l, local, p, tws, s, cr);
+  } else if (cudaMemsetAsync(local, 0, sizeof(F), s) != cudaSuccess) {
+    st = NRMF_ECUDA;
+  }
+  if (st != NRMF_OK) return st;
+  PeerArgs a{static_cast<char* const*>(peers), world, rank, err};
+  const int nr = (int)std::min<int64_t>(world, P2);
+  p2p_exchange_kernel<F><<<1, 32, 0, s>>>(local, a, nr, cr, out);
+  return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
+}
+
+template <typename F>
+int p2p_emulate(int world, const F* values, const void* peers, int flags, F* outs, void* stream) {
+  if (world < 1 || world > kP2PMaxRanks || !is_pow2(world) || !values || !peers || !outs) return NRMF_EINVAL;
+  PeerArgs a{static_cast<char* const*>(peers), world, 0, nullptr};
+  int nr = world;
+  int cr = flags & NRMF_TOP_CR;
+  void* args[] = {(void*)&values, (void*)&a, (void*)&nr, (void*)&cr, (void*)&outs};
+  if (cudaLaunchCooperativeKernel((void*)p2p_emulate_kernel<F>, dim3(world), dim3(32), args, 0,
+                                  static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return NRMF_ECUDA;
+  return NRMF_OK;
+}
+
 // ---------------------------------------------------------------- columns
 // Column blocks: rank r owns columns [t0, t1) of the canonical partition of
 // the P2c = pow2 >= cols column leaves of the Frobenius tree; its column norms
@@ -281,6 +349,63 @@ int nrmf_cols_dist_s(int64_t rows, int64_t cols_global, int64_t ld, int64_t col_
                      size_t ws_bytes, void* nccl_comm, void* stream) {
   return cols_dist_impl<float>(rows, cols_global, ld, col_offset, col_count, A_local, col_norms_local, frob,
                                flags, ws, ws_bytes, nccl_comm, stream);
+}
+
+size_t nrmf_p2p_buffer_bytes(void) { return (size_t)kP2PBytes; }
+
+int nrmf_p2p_alloc(void** buf) {
+  if (buf == nullptr) return NRMF_EINVAL;
+  void* p = nullptr;
+  if (cudaMalloc(&p, kP2PBytes) != cudaSuccess) return NRMF_ECUDA;
+  if (cudaMemset(p, 0, kP2PBytes) != cudaSuccess) {
+    cudaFree(p);
+    return NRMF_ECUDA;
+  }
+  *buf = p;
+  return NRMF_OK;
+}
+int nrmf_p2p_free(void* buf) { return cudaFree(buf) == cudaSuccess ? NRMF_OK : NRMF_ECUDA; }
+
+int nrmf_p2p_ipc_handle(const void* buf, char* handle64) {
+  if (buf == nullptr || handle64 == nullptr) return NRMF_EINVAL;
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(buf)) != cudaSuccess) return NRMF_ECUDA;
+  std::memcpy(handle64, &h, sizeof h);
+  return NRMF_OK;
+}
+int nrmf_p2p_open(const char* handle64, void** peer_buf) {
+  if (handle64 == nullptr || peer_buf == nullptr) return NRMF_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  if (cudaIpcOpenMemHandle(peer_buf, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return NRMF_ECUDA;
+  return NRMF_OK;
+}
+int nrmf_p2p_close(void* peer_buf) {
+  return cudaIpcCloseMemHandle(peer_buf) == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
+}
+
+int nrmf_dist_p2p_d(int64_t n_global, int64_t offset, int64_t count, const double* x_local, double* out,
+                    int flags, void* ws, size_t ws_bytes, const void* peers, int world, int rank, unsigned* err,
+                    void* stream) {
+  return dist_p2p_impl<double>(n_global, offset, count, x_local, out, flags, ws, ws_bytes, peers, world, rank,
+                               err, stream);
+}
+int nrmf_dist_p2p_s(int64_t n_global, int64_t offset, int64_t count, const float* x_local, float* out,
+                    int flags, void* ws, size_t ws_bytes, const void* peers, int world, int rank, unsigned* err,
+                    void* stream) {
+  return dist_p2p_impl<float>(n_global, offset, count, x_local, out, flags, ws, ws_bytes, peers, world, rank,
+                              err, stream);
+}
+
+// test hooks (not in nrmf.h): `world` ranks emulated as CTAs of one cooperative launch
+int nrmf_debug_p2p_emulate_d(int world, const double* values, const void* peers, int flags, double* outs,
+                             void* stream) {
+  return p2p_emulate<double>(world, values, peers, flags, outs, stream);
+}
+int nrmf_debug_p2p_emulate_s(int world, const float* values, const void* peers, int flags, float* outs,
+                             void* stream) {
+  return p2p_emulate<float>(world, values, peers, flags, outs, stream);
 }
 
 int nrmf_nccl_unique_id(char* id128) {
