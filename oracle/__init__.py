@@ -7,17 +7,31 @@ line-by-line citations).  Only ``tests/``, ``__graft_entry__.smoke()`` and
 package.  It shares no code with ``paper_2509_06220_b200`` (the product), and
 the product never imports it.
 
-Functions
-  v1_hypot(x, y, dtype)              Listing 2
-  R_H(x)                             Listing 1, literal
-  nrmf(x, lanes=None, J=None)        the tile-lane tree
+Functions (and what pins each, independently of this package)
+  v1_hypot(x, y, dtype)              Listing 2 -- exact-rational IEEE
+                                     re-implementation, closed forms, e:reH envelope
+  cr_hypot(x, y, dtype)              correctly rounded hypot (f1) -- exact rationals
+  R_H(x), R_A(x)                     Listing 1, literal, with v1 / cr
+                                     hypot -- e:r for n = 7, ceil splits
+  nrmf(x, lanes=None, J=None, top=)  the tile-lane tree -- lane
+                                     example P:912-932, one/two/three-hot vectors,
+                                     constants, scaling, zero/empty
   tiles(x, tau0, count)              tile values (sampled parity at full size)
-  cols(A, r, c, ld)                  column norms + Frobenius norm (e:F)
-  shard_norms(x, G)                  per-rank subtree values of the sharded tree
-  combine(values)                    R_H over a power-of-two padded list
+  cols(A, r, c, ld)                  column norms + Frobenius norm (e:F) -- column
+                                     == vector tree, frob == nrmf(vec A) at r = T
+  shard_ranges / shard_norms /       canonical shards and per-rank subtrees --
+  combine_ranks / combine            == the global tree for G = 1..8
+  cols_shard_ranges /                canonical column blocks and their Frobenius
+  cols_shard_frobs                   subtrees -- == the global frob for G = 1..8
   exact(x)                           exactly rounded RN(sqrt(sum x^2))
+                                     -- Python Fraction + isqrt, closed forms
   relerr(r, ref, dtype)              e:relerr (P:737-743)
-  ub_relerr_H(depth, dtype)          Thm 3 + e:reH upper bound for a depth-d tree
+  ub_relerr_H(depth, dtype)          Thm 3 + e:reH bound -- Table 3
+  bounds.py                          Thm 1-3 recurrences -- all 90 Table 3 values
+
+Parity unpinned: the absolute result values on random data -- the paper
+prints none; they are pinned only by the same-tree evaluation plus the bound
+against the exact reference.
 
 Tree constants (frozen, tree version 1): fp64 lanes=64, J=64; fp32 lanes=128,
 J=32; tile T = 4096.  These are restated here from DESIGN.md §3, not imported
