@@ -78,6 +78,11 @@ class ClockSampler:
             self.nv = None
             self.err = str(e)
             return self
+        try:   # board energy counter (mJ): average power over the timed region
+            self.e0 = self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)
+        except Exception:  # noqa: BLE001
+            self.e0 = None
+        self.t0 = time.perf_counter()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -103,6 +108,13 @@ class ClockSampler:
             time.sleep(self.period)
 
     def __exit__(self, *a):
+        self.t1 = time.perf_counter()
+        self.e1 = None
+        if getattr(self, "e0", None) is not None:
+            try:
+                self.e1 = self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)
+            except Exception:  # noqa: BLE001
+                self.e1 = None
         self._stop.set()
         if self._t:
             self._t.join()
@@ -111,8 +123,11 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                     "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        d = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+             "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if getattr(self, "e1", None) is not None and self.t1 > self.t0:
+            d["board_power_w"] = round((self.e1 - self.e0) * 1e-3 / (self.t1 - self.t0), 1)
+        return d
 
 
 # ------------------------------------------------------------------ helpers
@@ -319,6 +334,10 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": cnt * esz},
         "roofline_compute": compute_roofline(esz, cnt, kern_ms, f_ghz, hbm_peak),
     }
+    if clocks.get("board_power_w"):
+        # the FP64 kernel runs at the 1 kW board limit when sustained: its energy
+        # per step, not the clock it starts at, decides the sustained rate
+        line["energy_j_per_step"] = round(clocks["board_power_w"] * ms * 1e-3, 3)
     if allgather_us is not None:
         line["allgather_8B_us"] = allgather_us
     tr = load_traffic(esz)

@@ -299,6 +299,11 @@ struct StreamLoader {
     mbar_wait(my_s + L::kBars + (consumed % kStages) * 8, (consumed / kStages) & 1);
   }
   __device__ __forceinline__ void get_row(int, int row, F (&o)[Cfg<F>::V]) const {
+#ifdef NRMF_FAKE_SMEM  // dev-only energy/timing probe: leaves synthesized in registers (wrong results)
+#pragma unroll
+    for (int v = 0; v < Cfg<F>::V; ++v) o[v] = F(1) + F(row * 7 + v) * F(1e-3) + F(consumed & 3);
+    return;
+#endif
     const uint32_t addr = my_s + L::kRing + (consumed % kStages) * kBatchBytes + (threadIdx.x & 31) * 16 +
                           row * (kBatchBytes / kBatch);
     if constexpr (sizeof(F) == 8) {
