@@ -751,6 +751,7 @@ static int blocks_per_sm() {
 }
 
 static int g_grid_override = 0;  // test hook: force a grid size (0 = automatic)
+static int g_g0_override = -1;   // dev hook: force the warp-group level count g0 (-1 = automatic)
 
 // Launch the tree kernel over items (tiles) with mapping (tpc, ld, len).
 template <typename F>
@@ -789,17 +790,19 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   }
   // Warp-group size 2^g0 (<= 8 tiles).  The persistent warps take groups
   // round-robin, so the makespan is ceil(groups / W) groups of G tiles, and a
-  // group costs about G + 1/3 tiles (its cross-thread tail, announce and
-  // climb; measured at n = 2^26 / 2^28).  Take the G minimising
-  // ceil(groups / W) * (G + 1/3), the larger on ties.  The tree does not
-  // depend on g0.
+  // group costs about G + c tiles (its cross-thread tail, announce and climb:
+  // c = 1/3 fp64, 4/3 fp32 tiles, fitted to forced-g0 timings at n = 2^26..2^29
+  // with cool-downs, tools/g0_sweep.py).  Take the G minimising
+  // ceil(groups / W) * (G + c), the larger on ties.  The tree does not depend
+  // on g0.
   int g0_max = 0;
   {
     const int64_t W = grid * kWarps;
     double best = 0.0;
     for (int g = 3; g >= 0; --g) {
       const int64_t groups = (n_items + (int64_t(1) << g) - 1) >> g;
-      const double cost = (double)((groups + W - 1) / W) * ((double)(1 << g) + 1.0 / 3.0);
+      const double c = sizeof(F) == 8 ? 1.0 / 3.0 : 4.0 / 3.0;
+      const double cost = (double)((groups + W - 1) / W) * ((double)(1 << g) + c);
       if (g == 3 || cost < best - 1e-9) {
         best = cost;
         g0_max = g;
@@ -808,6 +811,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   }
   // without a combine (tile values only) the warp groups still batch the
   // cross-thread levels of their tiles; their group value is not used
+  if (g_g0_override >= 0) g0_max = g_g0_override;
   const Plan pl = combine ? make_plan(n_items, p2, g0_max)
                           : make_plan(n_items, int64_t(1) << g0_max, g0_max);
   const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
@@ -1159,6 +1163,11 @@ int nrmf_host_ex_s(int64_t n, const float* host_x, float* host_out, int flags, v
 }
 
 // test hook (not in nrmf.h): force the persistent grid size, 0 = automatic
+int nrmf_debug_set_g0(int g0) {
+  g_g0_override = (g0 < 0 || g0 > 3) ? -1 : g0;
+  return NRMF_OK;
+}
+
 int nrmf_debug_set_grid(int grid) {
   g_grid_override = grid < 0 ? 0 : grid;
   return NRMF_OK;

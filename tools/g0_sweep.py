@@ -1,0 +1,52 @@
+"""Dev tool: device time per warp-group size (forced g0) and size, to fit the
+group-size model of launch_tree."""
+import ctypes
+import random
+import statistics
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2509_06220_b200 as nrmf  # noqa: E402
+
+L = nrmf.lib()
+L.nrmf_debug_set_g0.argtypes = [ctypes.c_int]
+
+
+def t(x, reps=20):
+    out = torch.empty((), dtype=x.dtype, device="cuda")
+    g = nrmf.capture(lambda: nrmf.norm(x, out=out))
+    for _ in range(3):
+        g.replay()
+    ts = []
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+# measurements in random order, each after a 1.5 s cool-down (the FP64 kernel
+# is power-capped when hot), 3 repetitions -> minimum
+random.seed(1)
+cases = [(dt, lg, g0) for dt in (torch.float32, torch.float64) for lg in (26, 28, 29)
+         for g0 in (-1, 1, 2, 3) for _ in range(3)]
+random.shuffle(cases)
+xs = {}
+res = {}
+for dt, lg, g0 in cases:
+    key = (dt, lg)
+    if key not in xs:
+        xs[key] = torch.randn(1 << lg, dtype=dt, device="cuda")
+    L.nrmf_debug_set_g0(g0)
+    time.sleep(1.5)
+    v = t(xs[key], reps=5) * 1e3
+    res.setdefault((dt, lg, g0), []).append(v)
+L.nrmf_debug_set_g0(-1)
+for dt in (torch.float32, torch.float64):
+    for lg in (26, 28, 29):
+        r = {g0: min(res[(dt, lg, g0)]) for g0 in (-1, 1, 2, 3)}
+        print(f"{str(dt):14s} n=2^{lg}: auto {r[-1]:8.1f}  G2 {r[1]:8.1f}  G4 {r[2]:8.1f}  G8 {r[3]:8.1f} us",
+              flush=True)
