@@ -468,5 +468,12 @@ def _debug_set_grid(grid: int):
     _load().nrmf_debug_set_grid(grid)
 
 
+def _debug_set_g0(g0: int):
+    """Test hook: force the warp-group level count g0 in 0..3 (-1 = automatic)."""
+    L = _load()
+    L.nrmf_debug_set_g0.argtypes = [ctypes.c_int]
+    L.nrmf_debug_set_g0(g0)
+
+
 def build(force: bool = False) -> str:
     return _build.build(force=force)

@@ -237,6 +237,83 @@ __global__ void check_div_d_midpoints(uint64_t seed, uint64_t n, Counts* c) {
   atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
 }
 
+// Domain edges of the fast node: M within +-64 ulps of 2^-900 (lower edge),
+// 2^1012 (leaf bound) and 2^1021 (internal domain edge); q = m/M within +-64
+// ulps of 2^-69 (where the division sequence changes regime) and of 1.  A
+// leaf node (checked) must equal the exact node whenever it is not flagged;
+// an internal node (unchecked) must equal it whenever M is in the domain.
+__global__ void check_edges_d(uint64_t seed, uint64_t n, Counts* c) {
+  unsigned long long ck = 0, fa = 0, mi = 0;
+  const double edges[3] = {0x1p-900, 0x1p1012, 0x1p1021};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    const double e = edges[k % 3];
+    const double M = __longlong_as_double(__double_as_longlong(e) + (long long)((int)(mix(k) % 129) - 64));
+    double qt;
+    switch ((k >> 8) % 3) {
+      case 0: qt = __longlong_as_double(0x3ba0000000000000ll + (long long)((int)(mix(k + 1) % 129) - 64)); break;  // ~2^-69
+      case 1: qt = 1.0 - (double)(mix(k + 1) % 64) * 0x1p-53; break;                                             // ~1
+      default: qt = ldexp(1.0 + (double)(mix(k + 1) >> 12) * 0x1p-52, -(int)(mix(k + 2) % 80)); break;
+    }
+    const double m = __dmul_rn(M, qt);
+    const double x = (k >> 20) & 1 ? M : m, y = (k >> 20) & 1 ? m : M;
+    const double ex = v1h(x, y);
+    bool bad = false;
+    const double hl = v1h_fast<true>((k >> 21) & 1 ? -x : x, y, bad);    // leaf: signs allowed
+    ++ck;
+    if (!bad) {
+      ++fa;
+      if (__double_as_longlong(hl) != __double_as_longlong(ex)) ++mi;
+    }
+    const bool in = (unsigned)__double2hiint(fmax(x, y)) - kFastLoD < kFastSpanD;
+    if (in) {
+      const double a[1] = {x}, b[1] = {y};
+      double h[1];
+      bool d2 = false;
+      v1h_fast_n<false, 1>(a, b, h, d2);
+      if (__double_as_longlong(h[0]) != __double_as_longlong(ex)) ++mi;
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
+}
+
+__global__ void check_edges_s(uint64_t seed, uint64_t n, Counts* c) {
+  unsigned long long ck = 0, fa = 0, mi = 0;
+  const float edges[3] = {0x1p-80f, 0x1p116f, 0x1p125f};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    const float e = edges[k % 3];
+    const float M = __int_as_float(__float_as_int(e) + (int)(mix(k) % 129) - 64);
+    float qt;
+    switch ((k >> 8) % 3) {
+      case 0: qt = __int_as_float(0x39800000 + (int)(mix(k + 1) % 129) - 64); break;  // ~2^-12
+      case 1: qt = 1.0f - (float)(mix(k + 1) % 64) * 0x1p-24f; break;
+      default: qt = ldexpf(1.0f + (float)(mix(k + 1) >> 41) * 0x1p-23f, -(int)(mix(k + 2) % 40)); break;
+    }
+    const float m = __fmul_rn(M, qt);
+    const float x = (k >> 20) & 1 ? M : m, y = (k >> 20) & 1 ? m : M;
+    const float ex = v1h(x, y);
+    bool bad = false;
+    const float xs[2] = {(k >> 21) & 1 ? -x : x, y}, ys[2] = {y, x};
+    float hs[2];
+    v1h_fast_n<true, 2>(xs, ys, hs, bad);
+    ++ck;
+    if (!bad) {
+      ++fa;
+      if (__float_as_int(hs[0]) != __float_as_int(ex) || __float_as_int(hs[1]) != __float_as_int(ex)) ++mi;
+    }
+    const bool in = (unsigned)__float_as_int(fmaxf(x, y)) - kFastLoS < kFastSpanS;
+    if (in) {
+      const float a[2] = {x, y}, b[2] = {y, x};
+      float h[2];
+      bool d2 = false;
+      v1h_fast_n<false, 2>(a, b, h, d2);
+      if (__float_as_int(h[0]) != __float_as_int(ex) || __float_as_int(h[1]) != __float_as_int(ex)) ++mi;
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
+}
+
 extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long n, int mode,
                          unsigned long long* out3) {
   Counts* c;
@@ -251,6 +328,8 @@ extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long 
     case 5: check_internal_d<<<148 * 8, 256>>>(seed, n, c); break;
     case 6: check_internal_s<<<148 * 8, 256>>>(seed, n, c); break;
     case 7: check_div_d_midpoints<<<148 * 8, 256>>>(seed, n, c); break;
+    case 8: check_edges_d<<<148 * 8, 256>>>(seed, n, c); break;
+    case 9: check_edges_s<<<148 * 8, 256>>>(seed, n, c); break;
     default: return 2;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return 3;

@@ -90,3 +90,12 @@ def test_fp64_division_near_midpoints(fc):
     sequence equals __ddiv_rn on every one."""
     checked, _, mism = fc(7, seed=77, n=1 << 30)
     assert checked == 1 << 30 and mism == 0
+
+
+@pytest.mark.parametrize("which", [8, 9], ids=["fp64", "fp32"])
+def test_fast_domain_edges(fc, which):
+    """M within 64 ulps of every edge of the fast domain (2^-900 / 2^1012 /
+    2^1021; fp32 2^-80 / 2^116 / 2^125) and q near 2^-69 (2^-12) and near 1:
+    unflagged leaf nodes and in-domain internal nodes equal the exact node."""
+    checked, fast, mism = fc(which, seed=91 + which, n=1 << 26)
+    assert checked == 1 << 26 and mism == 0 and fast > 0

@@ -109,6 +109,27 @@ def test_reproducible_across_runs_and_grids(nrmf, dt):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("n", [8 * T * 3000 + 5, 2400 * T + 1, (1 << 24) + 3])
+def test_same_bits_for_every_group_size_and_grid(nrmf, dt, n):
+    """The tree does not depend on how tiles are batched into warp groups
+    (g0 = 0..3, i.e. 1, 2, 4, 8 tiles) nor on the persistent grid: every
+    combination gives the oracle's bits (stream kernel with full groups, a
+    partial last group and a ragged tail)."""
+    xh = gen.sme(n % 1000, n, dtype=dt)
+    x = dev(xh)
+    exp = bits(oracle.nrmf(xh), dt)
+    try:
+        for g0 in (0, 1, 2, 3):
+            nrmf._debug_set_g0(g0)
+            for grid in (0, 37, 148):
+                nrmf._debug_set_grid(grid)
+                assert bits(nrmf.norm(x).cpu().numpy(), dt) == exp, (g0, grid)
+    finally:
+        nrmf._debug_set_g0(-1)
+        nrmf._debug_set_grid(0)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_special_values(nrmf, dt):
     """Non-finite inputs follow Listing 2 literally on both sides (reading R4):
     inf anywhere -> inf; a NaN collapses to +0 when it meets a +0 leaf."""
