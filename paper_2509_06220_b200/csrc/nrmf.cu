@@ -427,16 +427,28 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         group_done = group_cross<F>(node, sl.my_s + WarpSmem<F>::kXs, G, job.top_cr, gv[0],
                                     job.tile_out != nullptr ? job.tile_out + grp * G : nullptr);
       if (!group_done) {
+        // exact path: the G tile values through the xs area, then the lg G
+        // group levels as a shuffle tree (contiguous pairs, the same tree)
+        const uint32_t xs = sl.my_s + WarpSmem<F>::kXs;
         for (int k = 0; k < G; ++k) {  // rolled
-          gv[0] = warp_tile_exact<F, kVec>(job.x + (grp * G + k) * (int64_t)kTile, kTile);
-          if (job.tile_out != nullptr && lane == 0) job.tile_out[grp * G + k] = gv[0];
-          if (G == 8) counter_merge<F, 1, 8>(k, gv, s0, s1, s2, ne);
-          else if (G == 4) counter_merge<F, 1, 4>(k, gv, s0, s1, s2, ne);
-          else if (G == 2) counter_merge<F, 1, 2>(k, gv, s0, s1, s2, ne);
+          const F tv = warp_tile_exact<F, kVec>(job.x + (grp * G + k) * (int64_t)kTile, kTile);
+          if (lane == 0) {
+            st_shared(xs + k * (uint32_t)sizeof(F), tv);
+            if (job.tile_out != nullptr) job.tile_out[grp * G + k] = tv;
+          }
         }
+        __syncwarp();
+        F v = F(0);
+        if (lane < G) ld_shared(xs + lane * (uint32_t)sizeof(F), v);
+        __syncwarp();
+        for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
+        gv[0] = v;
         group_done = true;
       }
     }
+    // the stream kernel merges a (partial) group's tile values through its xs
+    // area (groups of up to 16 tiles); the other kernels by counter_merge
+    const bool xs_merge = kStream && !group_done;
     for (int k = 0; k < G && !group_done; k += NT) {  // rolled
       F tv[NT];
       const F* bases[NT];
@@ -457,10 +469,22 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         const int64_t tau = grp * G + k + t;
         if (job.tile_out != nullptr && lane == 0 && tau < job.n_items) job.tile_out[tau] = tv[t];
         gv[0] = tv[t];
+        if (kStream) {
+          if (lane == 0) st_shared(sl.my_s + WarpSmem<F>::kXs + (k + t) * (uint32_t)sizeof(F), tv[t]);
+          continue;
+        }
         if (G == 8) counter_merge<F, 1, 8>(k + t, gv, s0, s1, s2, ne);
         else if (G == 4) counter_merge<F, 1, 4>(k + t, gv, s0, s1, s2, ne);
         else if (G == 2) counter_merge<F, 1, 2>(k + t, gv, s0, s1, s2, ne);
       }
+    }
+    if (kStream && xs_merge) {
+      __syncwarp();
+      F v = F(0);
+      if (lane < G) ld_shared(sl.my_s + WarpSmem<F>::kXs + lane * (uint32_t)sizeof(F), v);
+      __syncwarp();
+      for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
+      gv[0] = v;
     }
     if (!job.combine) continue;
     if (job.nsteps == 0) {  // the warp group is the whole tree
@@ -796,14 +820,17 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   // ceil(groups / W) * (G + c), the larger on ties.  The tree does not depend
   // on g0.
   int g0_max = 0;
+  // groups of up to kMaxGroup tiles on the stream kernel, 8 elsewhere
+  // (the column kernel's counter merge has three levels)
+  const int gmax = stream ? (sizeof(F) == 4 ? 4 : 3) : 3;
   {
     const int64_t W = grid * kWarps;
     double best = 0.0;
-    for (int g = 3; g >= 0; --g) {
+    for (int g = gmax; g >= 0; --g) {
       const int64_t groups = (n_items + (int64_t(1) << g) - 1) >> g;
       const double c = sizeof(F) == 8 ? 1.0 / 3.0 : 4.0 / 3.0;
       const double cost = (double)((groups + W - 1) / W) * ((double)(1 << g) + c);
-      if (g == 3 || cost < best - 1e-9) {
+      if (g == gmax || cost < best - 1e-9) {
         best = cost;
         g0_max = g;
       }
@@ -811,7 +838,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   }
   // without a combine (tile values only) the warp groups still batch the
   // cross-thread levels of their tiles; their group value is not used
-  if (g_g0_override >= 0) g0_max = g_g0_override;
+  if (g_g0_override >= 0) g0_max = std::min(g_g0_override, gmax);
   const Plan pl = combine ? make_plan(n_items, p2, g0_max)
                           : make_plan(n_items, int64_t(1) << g0_max, g0_max);
   const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
@@ -1164,7 +1191,7 @@ int nrmf_host_ex_s(int64_t n, const float* host_x, float* host_out, int flags, v
 
 // test hook (not in nrmf.h): force the persistent grid size, 0 = automatic
 int nrmf_debug_set_g0(int g0) {
-  g_g0_override = (g0 < 0 || g0 > 3) ? -1 : g0;
+  g_g0_override = (g0 < 0 || g0 > 4) ? -1 : g0;
   return NRMF_OK;
 }
 

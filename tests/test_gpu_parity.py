@@ -112,14 +112,15 @@ def test_reproducible_across_runs_and_grids(nrmf, dt):
 @pytest.mark.parametrize("n", [8 * T * 3000 + 5, 2400 * T + 1, (1 << 24) + 3])
 def test_same_bits_for_every_group_size_and_grid(nrmf, dt, n):
     """The tree does not depend on how tiles are batched into warp groups
-    (g0 = 0..3, i.e. 1, 2, 4, 8 tiles) nor on the persistent grid: every
+    (g0 = 0..4, i.e. 1..16 tiles; 16 on the fp32 stream kernel, clamped to 8
+    for fp64) nor on the persistent grid: every
     combination gives the oracle's bits (stream kernel with full groups, a
     partial last group and a ragged tail)."""
     xh = gen.sme(n % 1000, n, dtype=dt)
     x = dev(xh)
     exp = bits(oracle.nrmf(xh), dt)
     try:
-        for g0 in (0, 1, 2, 3):
+        for g0 in (0, 1, 2, 3, 4):
             nrmf._debug_set_g0(g0)
             for grid in (0, 37, 148):
                 nrmf._debug_set_grid(grid)

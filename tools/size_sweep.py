@@ -10,6 +10,9 @@ import torch
 sys.path.insert(0, ".")
 import paper_2509_06220_b200 as nrmf  # noqa: E402
 
+if len(sys.argv) > 1:            # time another build of the library
+    nrmf.LIB_PATH = sys.argv[1]
+
 
 def t(x, reps):
     out = torch.empty((), dtype=x.dtype, device="cuda")
