@@ -350,17 +350,18 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   constexpr bool kPipe = TMA && NRMF_USE_TMA;
   constexpr bool kStream = kPipe && STREAM && NT == 1;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)gridDim.x * kWarps;
+  // group and warp indices are 32-bit (a call has < 2^31 tiles: n < 2^43);
+  // fewer live 64-bit values leave more registers to the node chains
+  const int W = (int)gridDim.x * kWarps;
   // global warp index: CTA-major (a CTA streams kWarps consecutive groups)
   // when every warp has work; CTA-minor for calls with fewer groups than
   // warps, so that consecutive groups go to different SMs
-  const int64_t gw = job.cta_minor ? (int64_t)w * gridDim.x + blockIdx.x : (int64_t)blockIdx.x * kWarps + w;
+  const int gw = job.cta_minor ? w * (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x * kWarps + w;
   const int G = 1 << job.g0;
-  const int64_t n_groups = (job.n_items + G - 1) >> job.g0;
-  // vector mode: groups made only of full tiles
+  const int n_groups = (int)((job.n_items + G - 1) >> job.g0);
   // stream mode: warp groups made only of full tiles (tiles are contiguous:
   // a vector, or columns with ld == rows == a multiple of T)
-  const int64_t n_full = kStream ? (job.ld == 0 ? job.len / kTile : job.n_items) >> job.g0 : 0;
+  const int n_full = kStream ? (int)((job.ld == 0 ? job.len / kTile : job.n_items) >> job.g0) : 0;
 
   StreamLoader<F> sl;
   if (kStream) {
@@ -406,9 +407,9 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     for (int st = 0; st < kStages; ++st) pl.issue();
   }
 
-  int64_t pend_idx = -1;
+  int pend_idx = -1;
   unsigned pend_old = 0;
-  for (int64_t grp = gw; grp < n_groups; grp += W) {
+  for (int grp = gw; grp < n_groups; grp += W) {
     F s0[1], s1[1], s2[1], gv[1];
     NodeTop ne{job.top_cr};
     bool group_done = false;
@@ -783,6 +784,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
                        F* tile_out, F* out, int combine, void* ws, size_t ws_bytes, bool vec,
                        cudaStream_t s, int top_cr) {
   if (n_items == 0) return NRMF_OK;
+  if (n_items >= (int64_t(1) << 31) - 64) return NRMF_EINVAL;  // kernels index tiles/groups in 32 bits (n < 2^43)
   // contiguous tiles (a vector, or whole columns of T-multiple length stored
   // back to back): warp groups are contiguous, the pointer-walk producer applies
   const bool stream = vec && (ld == 0 || (ld == len && len % kTile == 0));
