@@ -407,8 +407,6 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     for (int st = 0; st < kStages; ++st) pl.issue();
   }
 
-  int pend_idx = -1;
-  unsigned pend_old = 0;
   for (int grp = gw; grp < n_groups; grp += W) {
     F s0[1], s1[1], s2[1], gv[1];
     NodeTop ne{job.top_cr};
@@ -492,18 +490,16 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
       if (lane == 0) *job.out = gv[0];
       continue;
     }
-    // announce this warp group (the counter result is consumed one group
-    // later, so the atomic's round trip overlaps the next group's arithmetic)
+    // announce this warp group; the last arriver of its 2^lg_fan group climbs.
+    // (Deferring the climb by one group to hide the atomic's round trip kept
+    // two more values live through the hot loop and was slower.)
     unsigned old = 0;
     if (lane == 0) {
       job.vals[job.val_off[0] + grp] = gv[0];
       old = atom_add_release(job.cnt + job.cnt_off[0] + (grp >> job.lg_fan[0]), 1u);
     }
-    if (pend_idx >= 0) climb(job, 0, pend_idx, pend_old);
-    pend_idx = grp;
-    pend_old = old;
+    climb(job, 0, grp, old);
   }
-  if (pend_idx >= 0) climb(job, 0, pend_idx, pend_old);
 }
 
 // Small calls (few tiles): one CTA per warp group of G tiles, and the NIT
