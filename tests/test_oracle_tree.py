@@ -296,3 +296,77 @@ def test_cols_block_shards_combine_to_global_frob(dt, r, c):
             vals = oracle.cols_shard_frobs(A, r, c, r, G)
             got = oracle.combine_ranks(vals)
             assert np.asarray(got, dtype=dt).tobytes() == np.asarray(efr, dtype=dt).tobytes(), (G, with_nan)
+
+
+# ------------------------------------------------------------ golden fixtures
+import os as _os
+import re as _re
+
+_GOLD = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "golden")
+
+
+def _golden(name):
+    out = {}
+    with open(_os.path.join(_GOLD, name)) as f:
+        for line in f:
+            line = line.split("#", 1)[0].strip()
+            if line:
+                k, v = line.split(":", 1)
+                out[k.strip()] = v.strip()
+    return out
+
+
+def _eval_tree(expr, env, bits):
+    """Evaluate h(a,b) / abs(a) / names with the exact-rational Listing 2."""
+    tok = _re.findall(r"[A-Za-z_][A-Za-z_0-9]*|[(),]", expr)
+    pos = 0
+
+    def parse():
+        nonlocal pos
+        t = tok[pos]
+        pos += 1
+        if t in ("h", "abs"):
+            assert tok[pos] == "("
+            pos += 1
+            a = parse()
+            if t == "abs":
+                assert tok[pos] == ")"
+                pos += 1
+                return abs(a)
+            assert tok[pos] == ","
+            pos += 1
+            b = parse()
+            assert tok[pos] == ")"
+            pos += 1
+            return H(a, b, bits)
+        return env[t]
+    v = parse()
+    assert pos == len(tok)
+    return v
+
+
+def test_golden_e_r_n7():
+    """tests/golden/e_r_n7.txt: the oracle's Listing 1 and the
+    one-lane tile tree with J = 8 evaluate exactly the transcribed tree."""
+    g = _golden("e_r_n7.txt")
+    for _ in range(50):
+        x = rng.uniform(-3, 3, 7)
+        env = {f"x{i + 1}": float(x[i]) for i in range(7)}
+        exp = _eval_tree(g["tree"], env, 64)
+        assert ie.same(float(oracle.R_H(x)), exp)
+        assert ie.same(float(oracle.nrmf(x, lanes=1, J=8)), exp)
+
+
+def test_golden_lane_example_p4_n16():
+    """tests/golden/lane_example_p4_n16.txt (P:912-932, P:962-967): the
+    oracle with p = 4 lanes, J = 4 is the transcribed lane trees + R."""
+    g = _golden("lane_example_p4_n16.txt")
+    for dt in (np.float64, np.float32):
+        b = BITS[dt]
+        for _ in range(20):
+            x = rng.uniform(-2, 2, 16).astype(dt)
+            env = {f"x{i + 1}": float(x[i]) for i in range(16)}
+            for l in range(1, 5):
+                env[f"lane{l}"] = _eval_tree(g[f"lane{l}"], env, b)
+            exp = _eval_tree(g["final"], env, b)
+            assert ie.same(float(oracle.nrmf(x, lanes=4, J=4)), exp, b)
