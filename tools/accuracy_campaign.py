@@ -72,9 +72,37 @@ def main():
             print(json.dumps(s), flush=True)
         del xd, host
         torch.cuda.empty_cache()
+    # the other BASELINE input families at their config sizes (north star:
+    # "within 64 eps of the exact norm on every config")
+    extra = [("f32", "sme (C2)", 1 << 28, lambda sd, n, out: gen.sme(sd, n, out=out), np.float32, args.runs),
+             ("f64", "extreme fin (C5)", 1 << 27, lambda sd, n, out: gen.extreme(sd, n, "fin", out=out), np.float64, 8),
+             ("f64", "extreme fin2 (C5)", 1 << 27, lambda sd, n, out: gen.extreme(sd, n, "fin2", out=out), np.float64, 8)]
+    for name, dist, ne, g, dt, runs in extra:
+        host = torch.empty(ne, dtype=torch.float64 if dt == np.float64 else torch.float32).pin_memory()
+        xh = host.numpy()
+        xd = torch.empty(ne, dtype=host.dtype, device="cuda")
+        errs = []
+        parity = None
+        for seed in range(1, runs + 1):
+            g(seed, ne, xh)
+            xd.copy_(host)
+            r = nrmf.norm(xd).item()
+            ex = oracle.exact(xh)
+            errs.append(oracle.relerr(r, ex, dt))
+            if seed == 1:
+                parity = bool(np.asarray(r, dtype=dt).tobytes() == np.asarray(oracle.nrmf(xh), dtype=dt).tobytes())
+        d = 12 + max(0, math.ceil(math.log2(max(1, -(-ne // T)))))
+        s = {"dtype": name, "dist": dist, "n": ne, "runs": runs, "relerr_eps_max": max(errs),
+             "relerr_eps_mean": statistics.mean(errs), "bound_thm3_eps": oracle.ub_relerr_H(d, dt),
+             "seed1_bit_exact_vs_oracle": parity}
+        res["series"].append(s)
+        print(json.dumps(s), flush=True)
+        del xd, host
+        torch.cuda.empty_cache()
     res["seconds"] = round(time.time() - t0, 1)
     res["paper_claim"] = "relerr < 3 eps for all recursive algorithms at n=2^29 (P:763-765)"
-    res["holds"] = all(s["relerr_eps_max"] < 3 for s in res["series"])
+    res["holds"] = all(s["relerr_eps_max"] < 3 for s in res["series"] if s.get("n", n) == n)
+    res["within_64eps_every_series"] = all(s["relerr_eps_max"] <= 64 for s in res["series"])
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(res, f, indent=1)

@@ -1,0 +1,34 @@
+"""Dev tool: randomized parity sweep -- N random sizes in [1, 2^24] (log-uniform),
+random dtype, distribution, pointer offset (alignment) and top, GPU vs the
+oracle bit for bit.  Complements the fixed-size tests."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import nrmf_inputs as gen  # noqa: E402
+import oracle  # noqa: E402
+import paper_2509_06220_b200 as nrmf  # noqa: E402
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 300
+rng = np.random.default_rng(2026)
+bad = 0
+for i in range(N):
+    n = int(np.exp(rng.uniform(0, np.log(1 << 24))))
+    dt = np.float64 if rng.integers(2) else np.float32
+    dist = ["normal", "uniform", "sme"][rng.integers(3)]
+    off = int(rng.integers(0, 4))           # elements of offset: 0 keeps 16-byte alignment only sometimes
+    top = "cr" if rng.integers(8) == 0 else "v1"
+    seed = int(rng.integers(1, 1 << 30))
+    m = n + off
+    x = {"normal": gen.normal, "uniform": gen.uniform_pm1, "sme": gen.sme}[dist](seed, m, dtype=dt)
+    xd = torch.from_numpy(x).cuda()[off:]
+    r = nrmf.norm(xd, top=top).cpu().numpy()
+    e = oracle.nrmf(x[off:], top=top)
+    ok = np.asarray(r, dtype=dt).tobytes() == np.asarray(e, dtype=dt).tobytes()
+    if not ok:
+        bad += 1
+        print("MISMATCH", n, dt.__name__, dist, off, top, seed, flush=True)
+print(f"{N} cases, {bad} mismatches")
+sys.exit(1 if bad else 0)
