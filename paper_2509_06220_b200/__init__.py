@@ -475,5 +475,12 @@ def _debug_set_g0(g0: int):
     L.nrmf_debug_set_g0(g0)
 
 
+def _debug_set_cta_step(on: bool):
+    """Test hook: the stream kernel's first combine step in shared memory (default on)."""
+    L = _load()
+    L.nrmf_debug_set_cta_step.argtypes = [ctypes.c_int]
+    L.nrmf_debug_set_cta_step(1 if on else 0)
+
+
 def build(force: bool = False) -> str:
     return _build.build(force=force)

@@ -36,12 +36,35 @@ constexpr int kMaxSteps = 8;
 #ifndef NRMF_USE_TMA
 #define NRMF_USE_TMA 1        // 0: aligned full tiles use direct LDG.128 instead of the TMA ring
 #endif
+#ifndef NRMF_CTA_STEP
+#define NRMF_CTA_STEP 1       // stream kernel: first combine step (16 warp groups) inside the CTA
+#endif
 #ifndef NRMF_MIN_BLOCKS
 #define NRMF_MIN_BLOCKS 1     // CTAs per SM the register allocation must allow (16 warps x 128 registers)
 #endif
 constexpr int kStages = NRMF_STAGES;
 constexpr int kBPI = NRMF_BPI;
 static_assert(kStages >= kBPI, "the ring must hold one iteration");
+
+#ifdef NRMF_PROBE_TRACE  // dev-only: globaltimer event trace of the tree kernel
+__device__ unsigned long long* g_trace = nullptr;
+__device__ unsigned g_trace_n = 0;
+__device__ unsigned g_trace_cap = 0;
+__device__ __forceinline__ void trace(unsigned type, unsigned level, unsigned id) {
+  if ((threadIdx.x & 31) != 0 || g_trace == nullptr) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const unsigned i = atomicAdd(&g_trace_n, 1u);
+  if (i < g_trace_cap) {
+    g_trace[2 * i] = ((unsigned long long)type << 56) | ((unsigned long long)level << 48) |
+                     ((unsigned long long)blockIdx.x << 24) | (threadIdx.x >> 5);
+    g_trace[2 * i + 1] = t;
+  }
+}
+#define NRMF_TRACE(a, b, c) trace(a, b, c)
+#else
+#define NRMF_TRACE(a, b, c) (void)0
+#endif
 
 // One evaluation of the tile tree.  Work unit of a warp: a "warp group" of
 // 2^g0 consecutive tiles (an aligned subtree: its first g0 levels are
@@ -63,6 +86,7 @@ struct TreeJob {
   int top_cr;          // levels above the tiles use cr_hypot (NRMF_TOP_CR)
   int g0;              // tile-tree levels combined inside a warp group (<= 3)
   int cta_minor;       // warp index w * gridDim + block (few groups) instead of block * kWarps + w
+  int cta_step0;       // stream kernel: step 0 (fan-in 16 = one CTA's warps of a round) in shared memory
   int nsteps;          // combine steps above the warp groups
   int lg_fan[kMaxSteps];
   int64_t nin[kMaxSteps];      // real (non-padding) inputs of step k (nin[0] = warp groups)
@@ -73,7 +97,7 @@ struct TreeJob {
 // One warp evaluates the balanced tree over 2^f (<= 64) consecutive values
 // vals[base ..] (entries >= nvals are +0).  All lanes return the value.
 template <typename F>
-__device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
+__device__ __forceinline__ F warp_group_bal_exact(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
   const int lane = threadIdx.x & 31;
   F v;
   int lv;
@@ -91,6 +115,38 @@ __device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_
   for (int l = 0; l < lv; ++l) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), cr);
   return v;
 }
+
+// The same subtree with fast nodes (v1_hypot top levels): a climb lies on the
+// kernel's critical path (the warp's next group waits for it, the last chain
+// of climbs is the kernel's tail), and the exact intrinsics' dependent chain
+// is ~5x longer.  A node whose larger operand is outside the fast domain (a
+// +0 pair of padding, inf, huge/tiny values) or a NaN result: the exact path.
+template <typename F>
+__device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
+  if (cr) return warp_group_bal_exact(vals, nvals, base, f, cr);
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  F v;
+  int lv;
+  if (f == 6) {
+    const int64_t i = base + 2 * lane;
+    const F a = i < nvals ? __ldcg(vals + i) : F(0);
+    const F b = i + 1 < nvals ? __ldcg(vals + i + 1) : F(0);
+    v = v1h_fast<true>(a, b, bad);
+    lv = 5;
+  } else {
+    const int64_t i = base + lane;
+    v = (lane < (1 << f) && i < nvals) ? __ldcg(vals + i) : F(0);
+    lv = f;
+  }
+  for (int l = 0; l < lv; ++l) v = v1h_fast<true>(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), bad);
+  // lanes >= 2^lv hold padding the result does not depend on
+  if (__any_sync(0xffffffffu, lane < (1 << lv) && (bad || v != v)))
+    return warp_group_bal_exact(vals, nvals, base, f, cr);
+  return v;
+}
+
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
   unsigned old;
@@ -113,9 +169,11 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
     const unsigned expect = (unsigned)(rem < fan ? rem : fan);
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != expect - 1) return;
-    __threadfence();  // acquire: the other arrivals' values are visible
+    NRMF_TRACE(2, k, 0);
+    fence_acq_rel_gpu();  // acquire: the other arrivals' values (released by their atomics) are visible
     if (lane == 0) job.cnt[job.cnt_off[k] + g] = 0u;  // ready for the next call
     const F v = warp_group_bal(job.vals + job.val_off[k], job.nin[k], g * fan, f, job.top_cr);
+    NRMF_TRACE(3, k, 0);
     if (k + 1 == job.nsteps) {
       if (lane == 0) *job.out = v;
       return;
@@ -248,6 +306,18 @@ struct PipeLoader {
   }
 };
 
+// CTA area of the stream kernel (after the kWarps warp blocks): the first
+// combine step in shared memory.  kCtaSlots rounds in flight: [values:
+// kCtaSlots x 16 F][arrival counters: kCtaSlots u32][round tags: kCtaSlots u32].
+constexpr int kCtaSlots = 4;
+template <typename F>
+struct CtaSmem {
+  static constexpr uint32_t kVals = 0;
+  static constexpr uint32_t kCnt = kCtaSlots * 16 * sizeof(F);
+  static constexpr uint32_t kTag = kCnt + kCtaSlots * 4;
+  static constexpr uint32_t kBytes = kTag + kCtaSlots * 4;
+};
+
 // Per-warp shared-memory block of the stream kernel (offsets from its base):
 // [ring: kStages x 4 KiB][stash][group thread values][mbarriers], 128-aligned.
 template <typename F>
@@ -258,6 +328,9 @@ struct WarpSmem {
   static constexpr uint32_t kBars = kXs + kGroupXsBytes<F>;
   static constexpr uint32_t kBytes = (kBars + kStages * 8 + 127) / 128 * 128;
 };
+static_assert(kWarps * WarpSmem<double>::kBytes + CtaSmem<double>::kBytes <= 227 * 1024 &&
+                  kWarps * WarpSmem<float>::kBytes + CtaSmem<float>::kBytes <= 227 * 1024,
+              "stream kernel shared memory");
 
 // Stream loader (contiguous tiles: a vector, or back-to-back columns of T
 // multiple length; 16-byte aligned): the batches of a full warp group (G
@@ -329,6 +402,107 @@ struct StreamLoader {
   }
 };
 
+// Step 0 of the combine inside the CTA (stream kernel, CTA-major warps): the
+// 16 warp groups of CTA-block b = grp >> 4 are the 16 warps' groups of one
+// round (grp & 15 == warp), an aligned subtree of 16 groups.  Each warp
+// deposits its group value in the round's shared-memory slot and counts in.
+// The block is then evaluated (4 levels, fast nodes with exact fallback) and
+// announced to the global step 1 -- not by its last arriver but by the first
+// warp to finish its NEXT round, which finds the slot complete and claims it:
+// the last arriver of a round is systematically the same, slowest warp of the
+// CTA (tools/trace_probe.py), and making it do the combine and the global
+// climbs on top delayed it by ~3 us per round; it ended the kernel ~50 us
+// after the others.  A warp without a next round claims at once (and the
+// round's completer either has a next round, where it will try, or claims at
+// once), so every round is claimed exactly once (CAS on the slot's tag).
+// Slot r % kCtaSlots serves round r + kCtaSlots after the claimer frees it
+// (tag r -> r|claimed -> r + kCtaSlots); a warp that far ahead waits.
+constexpr unsigned kClaimed = 0x80000000u;
+__device__ __forceinline__ unsigned ld_volatile_shared_u32(uint32_t a) {
+  unsigned v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_shared_u32(uint32_t a, unsigned v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_release_cta_shared(uint32_t a, unsigned v) {
+  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned cas_acq_rel_cta_shared(uint32_t a, unsigned cmp, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(v)
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acq_rel_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
+
+// Claim round rr's slot if complete and unclaimed; if claimed, evaluate CTA
+// block b and announce it to step 1 (climbing if last there).
+template <typename F>
+__device__ void cta_try(const TreeJob<F>& job, uint32_t cta_s, int rr, int b, int n_groups) {
+  using C = CtaSmem<F>;
+  const int lane = threadIdx.x & 31;
+  const uint32_t slot = (uint32_t)rr & (kCtaSlots - 1);
+  const uint32_t vs = cta_s + C::kVals + slot * 16 * (uint32_t)sizeof(F);
+  const uint32_t cs = cta_s + C::kCnt + slot * 4, ts = cta_s + C::kTag + slot * 4;
+  const int expect = n_groups - 16 * b < 16 ? n_groups - 16 * b : 16;
+  unsigned got = 0;
+  if (lane == 0 && ld_volatile_shared_u32(ts) == (unsigned)rr && ld_volatile_shared_u32(cs) == (unsigned)expect)
+    got = cas_acq_rel_cta_shared(ts, (unsigned)rr, (unsigned)rr | kClaimed) == (unsigned)rr;
+  if (!__shfl_sync(0xffffffffu, got, 0)) return;
+  fence_acq_rel_cta();  // every arrival's value is visible to every lane
+  NRMF_TRACE(2, 15, 0);
+  F v = F(0);
+  if (lane < expect) ld_shared(vs + lane * (uint32_t)sizeof(F), v);
+  bool bad = job.top_cr != 0;
+  if (!bad) {
+    F u = v;
+    for (int l = 0; l < 4; ++l) u = v1h_fast<true>(u, __shfl_xor_sync(0xffffffffu, u, 1 << l), bad);
+    bad = __any_sync(0xffffffffu, lane < 16 && (bad || u != u));  // lanes >= 16: padding, not used
+    if (!bad) v = u;
+  }
+  if (bad)
+    for (int l = 0; l < 4; ++l) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), job.top_cr);
+  __syncwarp();
+  if (lane == 0) {  // free the slot for round rr + kCtaSlots (its values are read)
+    st_shared_u32(cs, 0u);
+    fence_acq_rel_cta();
+    st_shared_u32(ts, (unsigned)(rr + kCtaSlots));
+  }
+  NRMF_TRACE(3, 15, 0);
+  if (job.nsteps == 1) {
+    if (lane == 0) *job.out = v;
+    return;
+  }
+  unsigned old1 = 0;
+  if (lane == 0) {
+    job.vals[job.val_off[1] + b] = v;
+    old1 = atom_add_release(job.cnt + job.cnt_off[1] + (b >> job.lg_fan[1]), 1u);
+  }
+  climb(job, 1, b, old1);
+}
+
+// Group grp (round r of this warp) has value gv: deposit it, then claim the
+// previous round and, without a next round, this one.
+template <typename F>
+__device__ __forceinline__ void cta_arrive(const TreeJob<F>& job, uint32_t cta_s, int grp, int r, int W, F gv,
+                                           int n_groups) {
+  using C = CtaSmem<F>;
+  const int lane = threadIdx.x & 31;
+  const uint32_t slot = (uint32_t)r & (kCtaSlots - 1);
+  if (lane == 0) {
+    const uint32_t ts = cta_s + C::kTag + slot * 4;
+    while (ld_volatile_shared_u32(ts) != (unsigned)r) __nanosleep(64);  // slot still serves round r - kCtaSlots
+    st_shared(cta_s + C::kVals + (slot * 16 + (grp & 15)) * (uint32_t)sizeof(F), gv);
+    red_add_release_cta_shared(cta_s + C::kCnt + slot * 4, 1u);
+  }
+  __syncwarp();
+  const int b = grp >> 4;
+  if (r >= 1) cta_try<F>(job, cta_s, r - 1, b - W / 16, n_groups);
+  if (grp + W >= n_groups) cta_try<F>(job, cta_s, r, b, n_groups);
+}
+
 // Value of tile tau when it is not part of a pipelined tuple: a full tile by
 // LDG (fast nodes, exact fallback), a partial one by the exact path, +0 for a
 // padding tile beyond the data.
@@ -381,6 +555,14 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     sl.skip_bytes = (W - 1) * G * (int64_t)kTile * (int64_t)sizeof(F);
     for (int st = 0; st < kStages; ++st) sl.issue(st);
   }
+  const uint32_t cta_s = smem_u32(smem) + kWarps * WarpSmem<F>::kBytes;
+  if (kStream && job.cta_step0) {
+    if (threadIdx.x < kCtaSlots) {
+      st_shared_u32(cta_s + CtaSmem<F>::kCnt + threadIdx.x * 4, 0u);
+      st_shared_u32(cta_s + CtaSmem<F>::kTag + threadIdx.x * 4, threadIdx.x);
+    }
+    __syncthreads();
+  }
 
   PipeLoader<F, NT> pl;
   if (kPipe && !kStream) {
@@ -407,7 +589,8 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     for (int st = 0; st < kStages; ++st) pl.issue();
   }
 
-  for (int grp = gw; grp < n_groups; grp += W) {
+  NRMF_TRACE(0, 0, 0);
+  for (int grp = gw, rnd = 0; grp < n_groups; grp += W, ++rnd) {
     F s0[1], s1[1], s2[1], gv[1];
     NodeTop ne{job.top_cr};
     bool group_done = false;
@@ -485,14 +668,21 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
       for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
       gv[0] = v;
     }
+    NRMF_TRACE(1, 0, 0);
     if (!job.combine) continue;
+#ifdef NRMF_PROBE_NO_ANNOUNCE  // dev-only timing probe: no announce/climb (wrong results)
+    if (lane == 0 && gv[0] == F(-1)) *job.out = gv[0];
+    continue;
+#endif
     if (job.nsteps == 0) {  // the warp group is the whole tree
       if (lane == 0) *job.out = gv[0];
       continue;
     }
+    if (kStream && job.cta_step0) {
+      cta_arrive<F>(job, cta_s, grp, rnd, W, gv[0], n_groups);
+      continue;
+    }
     // announce this warp group; the last arriver of its 2^lg_fan group climbs.
-    // (Deferring the climb by one group to hide the atomic's round trip kept
-    // two more values live through the hot loop and was slower.)
     unsigned old = 0;
     if (lane == 0) {
       job.vals[job.val_off[0] + grp] = gv[0];
@@ -500,6 +690,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     }
     climb(job, 0, grp, old);
   }
+  NRMF_TRACE(4, 0, 0);
 }
 
 // Small calls (few tiles): one CTA per warp group of G tiles, and the NIT
@@ -681,7 +872,7 @@ struct Plan {
   int64_t n_cnt = 0;
 };
 
-static Plan make_plan(int64_t n_items, int64_t p2, int g0_max) {
+static Plan make_plan(int64_t n_items, int64_t p2, int g0_max, int first_fan = 6) {
   Plan pl;
   int L = 0;
   while ((int64_t(1) << L) < p2) ++L;
@@ -690,7 +881,8 @@ static Plan make_plan(int64_t n_items, int64_t p2, int g0_max) {
   int64_t nin = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
   int64_t voff = 0, coff = 0;
   while (L > 0) {
-    const int f = L < 6 ? L : 6;
+    const int fmax = pl.nsteps == 0 ? first_fan : 6;
+    const int f = L < fmax ? L : fmax;
     const int k = pl.nsteps++;
     pl.lg_fan[k] = f;
     pl.nin[k] = nin;
@@ -709,8 +901,12 @@ static Plan make_plan(int64_t n_items, int64_t p2, int g0_max) {
 
 // Workspace of one tree evaluation: [counters][values] (worst case g0 = 0)
 static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
-  const Plan pl = make_plan(n_items, p2, 0);
-  return align_up((size_t)pl.n_cnt * 4, 256) + align_up((size_t)pl.n_vals * esz, 256) + 256;
+  size_t b = 0;
+  for (int ff : {6, 4}) {  // fan-in 64 first step, or 16 (the stream kernel's CTA step)
+    const Plan pl = make_plan(n_items, p2, 0, ff);
+    b = std::max(b, align_up((size_t)pl.n_cnt * 4, 256) + align_up((size_t)pl.n_vals * esz, 256) + 256);
+  }
+  return b;
 }
 
 template <typename F>
@@ -730,6 +926,7 @@ static TreeJob<F> make_job(const F* x, int64_t n_items, int64_t tpc, int64_t ld,
   job.top_cr = top_cr;
   job.g0 = pl.g0;
   job.cta_minor = 0;
+  job.cta_step0 = 0;
   job.nsteps = pl.nsteps;
   for (int k = 0; k < kMaxSteps; ++k) {
     job.lg_fan[k] = pl.lg_fan[k];
@@ -749,7 +946,7 @@ static TreeJob<F> make_job(const F* x, int64_t n_items, int64_t tpc, int64_t ld,
 template <typename F, bool TMA, bool STREAM = false>
 static size_t kernel_smem() {
   if (!(TMA && NRMF_USE_TMA)) return 0;
-  if (STREAM) return (size_t)kWarps * WarpSmem<F>::kBytes;
+  if (STREAM) return (size_t)kWarps * WarpSmem<F>::kBytes + CtaSmem<F>::kBytes;
   return (size_t)kWarps * kStages * kBatchBytes + (size_t)kWarps * kStages * 8;
 }
 
@@ -773,6 +970,7 @@ static int blocks_per_sm() {
 
 static int g_grid_override = 0;  // test hook: force a grid size (0 = automatic)
 static int g_g0_override = -1;   // dev hook: force the warp-group level count g0 (-1 = automatic)
+static int g_cta_step0 = NRMF_CTA_STEP;  // dev hook: first combine step in shared memory (stream kernel)
 
 // Launch the tree kernel over items (tiles) with mapping (tpc, ld, len).
 template <typename F>
@@ -837,8 +1035,19 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   // without a combine (tile values only) the warp groups still batch the
   // cross-thread levels of their tiles; their group value is not used
   if (g_g0_override >= 0) g0_max = std::min(g_g0_override, gmax);
-  const Plan pl = combine ? make_plan(n_items, p2, g0_max)
-                          : make_plan(n_items, int64_t(1) << g0_max, g0_max);
+  // stream kernel with every warp busy (CTA-major warps): the first combine
+  // step is the CTA's 16 warp groups of a round, in shared memory
+  Plan pl = combine ? make_plan(n_items, p2, g0_max)
+                    : make_plan(n_items, int64_t(1) << g0_max, g0_max);
+  bool cta_step0 = false;
+  if (stream && combine && kWarps == 16 && g_cta_step0 &&
+      ((n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0) >= grid * kWarps) {
+    const Plan p4 = make_plan(n_items, p2, g0_max, 4);
+    if (p4.nsteps >= 1 && p4.lg_fan[0] == 4 && p4.g0 == pl.g0) {
+      pl = p4;
+      cta_step0 = true;
+    }
+  }
   const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
   const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
   if (combine && ws_bytes < need) return NRMF_EWORKSPACE;
@@ -850,6 +1059,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   TreeJob<F> job = make_job(x, n_items, tpc, ld, len, tile_out, out, combine, top_cr, ws, cnt_bytes, pl);
   const int64_t n_groups = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
   job.cta_minor = n_groups < grid * kWarps;
+  job.cta_step0 = cta_step0 ? 1 : 0;
   grid = std::min<int64_t>(grid, n_groups);
   if (stream) {
     nrmf_tree_kernel<F, true, 1, true><<<(unsigned)grid, kThreads, kernel_smem<F, true, true>(), s>>>(job);
@@ -1188,8 +1398,24 @@ int nrmf_host_ex_s(int64_t n, const float* host_x, float* host_out, int flags, v
 }
 
 // test hook (not in nrmf.h): force the persistent grid size, 0 = automatic
+#ifdef NRMF_PROBE_TRACE
+int nrmf_debug_set_trace(void* buf, unsigned cap) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  unsigned z = 0;
+  if (cudaMemcpyToSymbol(nrmf::g_trace, &p, sizeof(p)) != cudaSuccess) return NRMF_ECUDA;
+  if (cudaMemcpyToSymbol(nrmf::g_trace_cap, &cap, sizeof(cap)) != cudaSuccess) return NRMF_ECUDA;
+  if (cudaMemcpyToSymbol(nrmf::g_trace_n, &z, sizeof(z)) != cudaSuccess) return NRMF_ECUDA;
+  return NRMF_OK;
+}
+#endif
+
 int nrmf_debug_set_g0(int g0) {
   g_g0_override = (g0 < 0 || g0 > 4) ? -1 : g0;
+  return NRMF_OK;
+}
+
+int nrmf_debug_set_cta_step(int on) {
+  g_cta_step0 = on != 0;
   return NRMF_OK;
 }
 

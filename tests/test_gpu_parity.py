@@ -131,6 +131,43 @@ def test_same_bits_for_every_group_size_and_grid(nrmf, dt, n):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("grid", [1, 2, 5])
+@pytest.mark.parametrize("case", ["normal", "nan_group", "zero_run", "huge_tiny", "cr"])
+def test_cta_combine_step(nrmf, dt, grid, case):
+    """The stream kernel's first combine step in shared memory (16 warp groups
+    of a round per CTA, claimed by the first warp to finish its next round):
+    small grids give many rounds per CTA (slot reuse beyond the 4 slots),
+    partial last blocks and a ragged tail; a NaN group, runs of +0 groups and
+    out-of-fast-domain group values take the exact fallback of that step;
+    top="cr" evaluates it with cr_hypot.  Same bits as the oracle, and as
+    with the step disabled (global fan-in-64 climbs only)."""
+    G = 16 if dt == np.float32 else 8
+    n = grid * 16 * G * T * 9 + 5 * G * T + 3 * T + 17      # 9 full rounds, a partial one, ragged tail
+    xh = gen.normal(grid * 7 + len(case), n, dtype=dt)
+    if case == "nan_group":
+        xh[3 * G * T + 5] = np.nan
+    elif case == "zero_run":
+        xh[: 40 * G * T] = 0
+    elif case == "huge_tiny":
+        # group values above / below the fast node's domain of M
+        # ([2^-900, 2^1012) fp64, [2^-80, 2^116) fp32): one large group, 16 tiny
+        big, tiny = (2.0 ** 1010, 2.0 ** -950) if dt == np.float64 else (2.0 ** 110, 2.0 ** -100)
+        xh[G * T * 17: G * T * 18] *= dt(big)
+        xh[G * T * 40: G * T * 56] *= dt(tiny)
+    top = "cr" if case == "cr" else "v1"
+    exp = bits(oracle.nrmf(xh, top=top), dt)
+    x = dev(xh)
+    try:
+        nrmf._debug_set_grid(grid)
+        for on in (True, False):
+            nrmf._debug_set_cta_step(on)
+            assert bits(nrmf.norm(x, top=top).cpu().numpy(), dt) == exp, on
+    finally:
+        nrmf._debug_set_cta_step(True)
+        nrmf._debug_set_grid(0)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_special_values(nrmf, dt):
     """Non-finite inputs follow Listing 2 literally on both sides (reading R4):
     inf anywhere -> inf; a NaN collapses to +0 when it meets a +0 leaf."""

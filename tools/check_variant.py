@@ -1,5 +1,6 @@
 """Dev tool: bit-compare a libnrmf.so variant with the oracle on a few inputs."""
 import ctypes
+import os
 import sys
 
 import numpy as np
@@ -17,7 +18,10 @@ L.nrmf_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
 L.nrmf_workspace_bytes.restype = ctypes.c_size_t
 bad = 0
 for dt, f in ((np.float64, L.nrmf_d), (np.float32, L.nrmf_s)):
-    for n in (4096, 5 * 4096 + 3, 300 * 4096 + 77, (1 << 22) + 5):
+    sizes = [4096, 5 * 4096 + 3, 300 * 4096 + 77, (1 << 22) + 5]
+    if os.environ.get("BIG"):  # persistent-kernel sizes (every warp busy, several rounds, ragged ends)
+        sizes += [(1 << 25) + 3 * 4096 + 5, 37 * 16 * 2368 * 4096 // 16 + 4095, (1 << 28) + 12345, 1 << 30]
+    for n in sizes:
         x = gen.normal(n, n, dtype=dt)
         xd = torch.from_numpy(x).cuda()
         out = torch.empty((), dtype=xd.dtype, device="cuda")

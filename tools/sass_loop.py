@@ -48,7 +48,9 @@ def main():
             if m and int(m.group(1), 16) < a:
                 lo, hi = int(m.group(1), 16), a
                 body = [x for x in ins if lo <= x[0] <= hi]
-                if any("LDS" in x[1] for x in body):
+                # the leaf loop reads the ring with vector LDS (.64/.128);
+                # short spin loops on a shared-memory word do not count
+                if any(re.search(r"\bLDS\.(64|128)", x[1]) for x in body):
                     loops.append((hi - lo, lo, hi, body))
         if not loops:
             print(name, "no LDS loop")
