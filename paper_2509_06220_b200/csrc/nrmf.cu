@@ -1011,8 +1011,9 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   // Warp-group size 2^g0 (<= 8 tiles).  The persistent warps take groups
   // round-robin, so the makespan is ceil(groups / W) groups of G tiles, and a
   // group costs about G + c tiles (its cross-thread tail, announce and climb:
-  // c = 1/3 fp64, 4/3 fp32 tiles, fitted to forced-g0 timings at n = 2^26..2^29
-  // with cool-downs, tools/g0_sweep.py).  Take the G minimising
+  // c = 1/3 tile, fitted to forced-g0 timings at n = 2^26..2^30 with
+  // cool-downs, tools/g0_sweep.py; fp32 was 4/3 before the CTA combine step
+  // made the announce cheap: fp32 2^28 now runs G = 4, 190 -> 180 us).  Take the G minimising
   // ceil(groups / W) * (G + c), the larger on ties.  The tree does not depend
   // on g0.
   int g0_max = 0;
@@ -1024,7 +1025,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
     double best = 0.0;
     for (int g = gmax; g >= 0; --g) {
       const int64_t groups = (n_items + (int64_t(1) << g) - 1) >> g;
-      const double c = sizeof(F) == 8 ? 1.0 / 3.0 : 4.0 / 3.0;
+      const double c = 1.0 / 3.0;
       const double cost = (double)((groups + W - 1) / W) * ((double)(1 << g) + c);
       if (g == gmax || cost < best - 1e-9) {
         best = cost;

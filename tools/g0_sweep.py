@@ -32,7 +32,8 @@ def t(x, reps=20):
 # is power-capped when hot), 3 repetitions -> minimum
 random.seed(1)
 G0S = (-1, 1, 2, 3, 4)
-cases = [(dt, lg, g0) for dt in (torch.float32,) for lg in (26, 28, 29, 30)
+DTS = (torch.float32, torch.float64) if "--both" in sys.argv else (torch.float32,)
+cases = [(dt, lg, g0) for dt in DTS for lg in (26, 28, 29, 30)
          for g0 in G0S for _ in range(3)]
 random.shuffle(cases)
 xs = {}
@@ -46,7 +47,7 @@ for dt, lg, g0 in cases:
     v = t(xs[key], reps=5) * 1e3
     res.setdefault((dt, lg, g0), []).append(v)
 L.nrmf_debug_set_g0(-1)
-for dt in (torch.float32,):
+for dt in DTS:
     for lg in (26, 28, 29, 30):
         r = {g0: min(res[(dt, lg, g0)]) for g0 in G0S}
         print(f"{str(dt):14s} n=2^{lg}: auto {r[-1]:8.1f}  G2 {r[1]:8.1f}  G4 {r[2]:8.1f}  G8 {r[3]:8.1f}"
