@@ -168,6 +168,30 @@ def test_cta_combine_step(nrmf, dt, grid, case):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("rows", [T, 2 * T])
+def test_cta_combine_step_columns(nrmf, dt, rows):
+    """Back-to-back columns of a multiple of T rows take the stream kernel
+    (tile values = column norms written by the group step): with a grid of 2
+    CTAs it runs many rounds through the CTA combine step.  Column norms and
+    the Frobenius norm equal the oracle's, with the step on and off."""
+    G = 16 if dt == np.float32 else 8
+    c = (2 * 16 * G * 5 + 3 * G + 1) * T // rows
+    A = gen.colscaled_normal(11, rows, c, ld=rows, dtype=dt)
+    At = dev(A).as_strided((rows, c), (1, rows))
+    ecol, efr = oracle.cols(A, rows, c, rows)
+    try:
+        nrmf._debug_set_grid(2)
+        for on in (True, False):
+            nrmf._debug_set_cta_step(on)
+            col, fr = nrmf.cols(At)
+            assert col.cpu().numpy().tobytes() == ecol.tobytes(), on
+            assert bits(fr.cpu().numpy(), dt) == bits(efr, dt), on
+    finally:
+        nrmf._debug_set_cta_step(True)
+        nrmf._debug_set_grid(0)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_special_values(nrmf, dt):
     """Non-finite inputs follow Listing 2 literally on both sides (reading R4):
     inf anywhere -> inf; a NaN collapses to +0 when it meets a +0 leaf."""
