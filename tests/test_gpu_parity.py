@@ -168,6 +168,28 @@ def test_cta_combine_step(nrmf, dt, grid, case):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("top", ["v1", "cr"])
+@pytest.mark.parametrize("extra", [0, 5])
+def test_cta_combine_step_is_root(nrmf, dt, top, extra):
+    """One CTA (grid 1) and exactly 16 warp groups (+ a few elements of a 17th
+    group when extra > 0, which adds a global step): the CTA step writes the
+    root itself, or feeds the global step."""
+    G = 16 if dt == np.float32 else 8
+    n = 16 * G * T + extra
+    xh = gen.uniform_pm1(n, n, dtype=dt)
+    exp = bits(oracle.nrmf(xh, top=top), dt)
+    x = dev(xh)
+    try:
+        nrmf._debug_set_grid(1)
+        for on in (True, False):
+            nrmf._debug_set_cta_step(on)
+            assert bits(nrmf.norm(x, top=top).cpu().numpy(), dt) == exp, on
+    finally:
+        nrmf._debug_set_cta_step(True)
+        nrmf._debug_set_grid(0)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 @pytest.mark.parametrize("rows", [T, 2 * T])
 def test_cta_combine_step_columns(nrmf, dt, rows):
     """Back-to-back columns of a multiple of T rows take the stream kernel
