@@ -1008,14 +1008,15 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
       return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
     }
   }
-  // Warp-group size 2^g0 (<= 8 tiles).  The persistent warps take groups
-  // round-robin, so the makespan is ceil(groups / W) groups of G tiles, and a
-  // group costs about G + c tiles (its cross-thread tail, announce and climb:
-  // c = 1/3 tile, fitted to forced-g0 timings at n = 2^26..2^30 with
-  // cool-downs, tools/g0_sweep.py; fp32 was 4/3 before the CTA combine step
-  // made the announce cheap: fp32 2^28 now runs G = 4, 190 -> 180 us).  Take the G minimising
-  // ceil(groups / W) * (G + c), the larger on ties.  The tree does not depend
-  // on g0.
+  // Warp-group size G = 2^g0 (<= 8 tiles; 16 for fp32 on the stream kernel).
+  // The persistent warps take groups round-robin, so the makespan is
+  // ceil(groups / W) groups of G tiles, and a group costs about G + c tiles
+  // (its cross-thread tail and announce: c = 1/3 tile, fitted to forced-g0
+  // timings at n = 2^26..2^30 with cool-downs, tools/g0_sweep.py; fp32 was
+  // 4/3 before the CTA combine step made the announce cheap: fp32 2^28 now
+  // runs G = 4, 190 -> 180 us).  Take the G minimising ceil(groups / W) *
+  // (G + c), the larger on ties.  The tree does not depend on g0.
+  constexpr double kGroupCost = 1.0 / 3.0;
   int g0_max = 0;
   // groups of up to kMaxGroup tiles on the stream kernel, 8 elsewhere
   // (the column kernel's counter merge has three levels)
@@ -1025,8 +1026,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
     double best = 0.0;
     for (int g = gmax; g >= 0; --g) {
       const int64_t groups = (n_items + (int64_t(1) << g) - 1) >> g;
-      const double c = 1.0 / 3.0;
-      const double cost = (double)((groups + W - 1) / W) * ((double)(1 << g) + c);
+      const double cost = (double)((groups + W - 1) / W) * ((double)(1 << g) + kGroupCost);
       if (g == gmax || cost < best - 1e-9) {
         best = cost;
         g0_max = g;
