@@ -27,6 +27,7 @@ namespace nrmf {
 
 // ------------------------------------------------------------------ kernels
 constexpr int kMaxSteps = 8;
+constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's last one up to 8 (fan-in 256)
 #ifndef NRMF_STAGES
 #define NRMF_STAGES 2         // TMA ring depth per warp (batches of 4 KiB)
 #endif
@@ -94,10 +95,14 @@ struct TreeJob {
   int64_t cnt_off[kMaxSteps];  // cnt offset of the counters of step k
 };
 
-// One warp evaluates the balanced tree over 2^f (<= 64) consecutive values
-// vals[base ..] (entries >= nvals are +0).  All lanes return the value.
+// One warp evaluates the balanced tree over 2^f (f <= kMaxFanLg) consecutive
+// values vals[base ..] (entries >= nvals are +0).  All lanes return the value.
+// Exact nodes (IEEE intrinsics or cr_hypot): f <= 6 in one pass (lane l
+// takes values 2l, 2l+1 when f = 6), f = 7, 8 as the top levels over 64-value
+// subtrees (the same tree; split kernel only).  That part is not inlined:
+// inlined, its calls and live values grew the stack frame 80 -> 400 bytes.
 template <typename F>
-__device__ __forceinline__ F warp_group_bal_exact(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
+__device__ __forceinline__ F warp_bal_exact6(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
   const int lane = threadIdx.x & 31;
   F v;
   int lv;
@@ -115,25 +120,62 @@ __device__ __forceinline__ F warp_group_bal_exact(const F* vals, int64_t nvals, 
   for (int l = 0; l < lv; ++l) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), cr);
   return v;
 }
+template <typename F>
+__device__ __noinline__ F warp_bal_exact_wide(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
+  const F a = warp_bal_exact6<F>(vals, nvals, base, 6, cr);
+  const F b = warp_bal_exact6<F>(vals, nvals, base + 64, 6, cr);
+  const F l = top_node<F>(a, b, cr);
+  if (f == 7) return l;
+  const F c = warp_bal_exact6<F>(vals, nvals, base + 128, 6, cr);
+  const F d = warp_bal_exact6<F>(vals, nvals, base + 192, 6, cr);
+  return top_node<F>(l, top_node<F>(c, d, cr), cr);
+}
+template <typename F, bool WIDE>
+__device__ __forceinline__ F warp_group_bal_exact(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
+  if (WIDE && f > 6) return warp_bal_exact_wide<F>(vals, nvals, base, f, cr);
+  return warp_bal_exact6<F>(vals, nvals, base, f, cr);
+}
+
+// Fast-node version: f >= 5: lane l takes the K = 2^(f-5) contiguous values
+// [lK, lK+K) as an in-register tree, then 5 __shfl_xor levels; f < 5: lanes
+// < 2^f one value each, f shuffle levels.  `bad` flags a node outside the
+// fast domain; lv = the shuffle levels.
+template <typename F, int K>
+__device__ __forceinline__ F lane_bal_fast(const F* vals, int64_t nvals, int64_t base, bool& bad) {
+  const int lane = threadIdx.x & 31;
+  F a[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int64_t i = base + (int64_t)K * lane + j;
+    a[j] = i < nvals ? __ldcg(vals + i) : F(0);
+  }
+#pragma unroll
+  for (int st = 1; st < K; st <<= 1)
+#pragma unroll
+    for (int j = 0; j < K; j += 2 * st) a[j] = v1h_fast<true>(a[j], a[j + st], bad);
+  return a[0];
+}
 
 // The same subtree with fast nodes (v1_hypot top levels): a climb lies on the
 // kernel's critical path (the warp's next group waits for it, the last chain
 // of climbs is the kernel's tail), and the exact intrinsics' dependent chain
 // is ~5x longer.  A node whose larger operand is outside the fast domain (a
 // +0 pair of padding, inf, huge/tiny values) or a NaN result: the exact path.
-template <typename F>
+// WIDE: steps of up to 8 levels (the split kernel's plans); otherwise <= 6.
+template <typename F, bool WIDE>
 __device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_t base, int f, int cr) {
-  if (cr) return warp_group_bal_exact(vals, nvals, base, f, cr);
+  if (cr) return warp_group_bal_exact<F, WIDE>(vals, nvals, base, f, cr);
   const int lane = threadIdx.x & 31;
   bool bad = false;
   F v;
-  int lv;
-  if (f == 6) {
+  int lv = 5;
+  if (WIDE && f == 8) v = lane_bal_fast<F, 8>(vals, nvals, base, bad);
+  else if (WIDE && f == 7) v = lane_bal_fast<F, 4>(vals, nvals, base, bad);
+  else if (f == 6) {
     const int64_t i = base + 2 * lane;
     const F a = i < nvals ? __ldcg(vals + i) : F(0);
     const F b = i + 1 < nvals ? __ldcg(vals + i + 1) : F(0);
     v = v1h_fast<true>(a, b, bad);
-    lv = 5;
   } else {
     const int64_t i = base + lane;
     v = (lane < (1 << f) && i < nvals) ? __ldcg(vals + i) : F(0);
@@ -142,7 +184,7 @@ __device__ __forceinline__ F warp_group_bal(const F* vals, int64_t nvals, int64_
   for (int l = 0; l < lv; ++l) v = v1h_fast<true>(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), bad);
   // lanes >= 2^lv hold padding the result does not depend on
   if (__any_sync(0xffffffffu, lane < (1 << lv) && (bad || v != v)))
-    return warp_group_bal_exact(vals, nvals, base, f, cr);
+    return warp_group_bal_exact<F, WIDE>(vals, nvals, base, f, cr);
   return v;
 }
 
@@ -158,7 +200,7 @@ __device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
 // with counter value `old`.  If this warp was the last arrival of its group,
 // evaluate the group's subtree and climb.  Last-arriver combine: who computes
 // a node depends on timing, what is computed never does.
-template <typename F>
+template <typename F, bool WIDE = false>
 __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
   const int lane = threadIdx.x & 31;
   while (true) {
@@ -172,7 +214,7 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
     NRMF_TRACE(2, k, 0);
     fence_acq_rel_gpu();  // acquire: the other arrivals' values (released by their atomics) are visible
     if (lane == 0) job.cnt[job.cnt_off[k] + g] = 0u;  // ready for the next call
-    const F v = warp_group_bal(job.vals + job.val_off[k], job.nin[k], g * fan, f, job.top_cr);
+    const F v = warp_group_bal<F, WIDE>(job.vals + job.val_off[k], job.nin[k], g * fan, f, job.top_cr);
     NRMF_TRACE(3, k, 0);
     if (k + 1 == job.nsteps) {
       if (lane == 0) *job.out = v;
@@ -714,6 +756,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   const int G = 1 << job.g0;
   const int64_t grp = blockIdx.x;
   const int k = w / NIT, it = w % NIT;
+  NRMF_TRACE(0, 0, 0);
   // are all G tiles of the group full tiles with data?
   bool full = (grp + 1) * G <= job.n_items;
   for (int t = 0; t < G && full; ++t) {
@@ -736,6 +779,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     batch_lanes<F>(ld, node, r);
     st_stash(smem_u32(stash) + ((k * NIT + it) * 32 + lane) * 16, r);
     if (__any_sync(0xffffffffu, node.bad) && lane == 0) s_bad = 1;
+    NRMF_TRACE(5, 0, 0);
   }
   __syncthreads();
   if (w != 0) return;
@@ -766,6 +810,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     }
     gv = g[0];
   }
+  NRMF_TRACE(1, 0, 0);
   if (!job.combine) return;
   if (job.nsteps == 0) {
     if (lane == 0) *job.out = gv;
@@ -776,7 +821,8 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     job.vals[job.val_off[0] + grp] = gv;
     old = atom_add_release(job.cnt + job.cnt_off[0] + (grp >> job.lg_fan[0]), 1u);
   }
-  climb(job, 0, grp, old);
+  climb<F, true>(job, 0, grp, old);
+  NRMF_TRACE(4, 0, 0);
 }
 
 // Balanced tree over vals[0..P) (entries >= nvals are +0) -> *out.  One CTA.
@@ -860,7 +906,9 @@ static int device_sms() {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // Plan of the combine over p2 tiles of which n_items are real: g0 levels
-// inside each warp group, then steps of up to 6 levels (fan-in 64).
+// inside each warp group, then steps of 6 levels (fan-in 64); first_fan = 4:
+// the first step is the stream kernel's CTA step; last_fan = 8: the last step
+// may take up to 8 levels (split kernel).
 struct Plan {
   int g0 = 0;
   int nsteps = 0;
@@ -872,7 +920,7 @@ struct Plan {
   int64_t n_cnt = 0;
 };
 
-static Plan make_plan(int64_t n_items, int64_t p2, int g0_max, int first_fan = 6) {
+static Plan make_plan(int64_t n_items, int64_t p2, int g0_max, int first_fan = 6, int last_fan = 6) {
   Plan pl;
   int L = 0;
   while ((int64_t(1) << L) < p2) ++L;
@@ -881,7 +929,12 @@ static Plan make_plan(int64_t n_items, int64_t p2, int g0_max, int first_fan = 6
   int64_t nin = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
   int64_t voff = 0, coff = 0;
   while (L > 0) {
-    const int fmax = pl.nsteps == 0 ? first_fan : 6;
+    // steps of 6 levels (fan-in 64); with last_fan = 8 (the split kernel)
+    // the last step may take up to 8: one climb of 8 levels instead of two
+    // climbs and an atomic round trip in between (C1, 2^20 fp64: 13.3 ->
+    // 12.4 us).  In the persistent kernel the wider climb code cost 0.3-0.8 %
+    // at 2^24..2^30 (tools/size_sweep.py A/B), so it stays at 6 there.
+    const int fmax = pl.nsteps == 0 && first_fan < 6 ? first_fan : (L <= last_fan ? L : 6);
     const int f = L < fmax ? L : fmax;
     const int k = pl.nsteps++;
     pl.lg_fan[k] = f;
@@ -902,8 +955,8 @@ static Plan make_plan(int64_t n_items, int64_t p2, int g0_max, int first_fan = 6
 // Workspace of one tree evaluation: [counters][values] (worst case g0 = 0)
 static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
   size_t b = 0;
-  for (int ff : {6, 4}) {  // fan-in 64 first step, or 16 (the stream kernel's CTA step)
-    const Plan pl = make_plan(n_items, p2, 0, ff);
+  for (int ff : {6, 4, 8}) {  // fan-in 64 steps, a first CTA step of 16, or a last step up to 256
+    const Plan pl = ff == 8 ? make_plan(n_items, p2, 0, 6, 8) : make_plan(n_items, p2, 0, ff);
     b = std::max(b, align_up((size_t)pl.n_cnt * 4, 256) + align_up((size_t)pl.n_vals * esz, 256) + 256);
   }
   return b;
@@ -996,7 +1049,8 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
     if (!combine) g0s = 0;
     const int64_t n_groups = (n_items + (int64_t(1) << g0s) - 1) >> g0s;
     if (g_grid_override == 0 && n_groups <= 4 * (int64_t)device_sms()) {
-      const Plan pl = combine ? make_plan(n_items, p2, g0s) : make_plan(n_items, int64_t(1) << g0s, g0s);
+      const Plan pl = combine ? make_plan(n_items, p2, g0s, 6, kMaxFanLg)
+                              : make_plan(n_items, int64_t(1) << g0s, g0s);
       const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
       const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
       if (combine && ws_bytes < need) return NRMF_EWORKSPACE;

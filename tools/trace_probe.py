@@ -48,7 +48,8 @@ def main():
         wid = (a[:, 0] & ((1 << 48) - 1)).astype(np.int64)
         t = (a[:, 1] - a[:, 1].min()).astype(np.int64) / 1e3  # us
         print(f"== {dt} n=2^{lg}: event-timed {ms * 1e3:.1f} us, {len(a)} events")
-        for k, name in ((0, "start"), (1, "group end"), (2, "climb start"), (3, "climb end"), (4, "exit")):
+        for k, name in ((0, "start"), (5, "batch end"), (1, "group end"), (2, "climb start"), (3, "climb end"),
+                        (4, "exit")):
             tk = t[typ == k]
             if len(tk):
                 print(f"  {name:12s} n={len(tk):6d} min {tk.min():8.1f} med {np.median(tk):8.1f} "
