@@ -1,6 +1,7 @@
 """Dev tool: randomized parity sweep -- N random sizes in [1, 2^24] (log-uniform),
-random dtype, distribution, pointer offset (alignment) and top, GPU vs the
-oracle bit for bit.  Complements the fixed-size tests."""
+random dtype, distribution, pointer offset (alignment) and top, and (with
+--launch) random persistent-grid size, warp-group size and CTA combine step
+on/off; GPU vs the oracle bit for bit.  Complements the fixed-size tests."""
 import sys
 
 import numpy as np
@@ -11,7 +12,8 @@ import nrmf_inputs as gen  # noqa: E402
 import oracle  # noqa: E402
 import paper_2509_06220_b200 as nrmf  # noqa: E402
 
-N = int(sys.argv[1]) if len(sys.argv) > 1 else 300
+N = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 300
+LAUNCH = "--launch" in sys.argv
 rng = np.random.default_rng(2026)
 bad = 0
 for i in range(N):
@@ -24,11 +26,24 @@ for i in range(N):
     m = n + off
     x = {"normal": gen.normal, "uniform": gen.uniform_pm1, "sme": gen.sme}[dist](seed, m, dtype=dt)
     xd = torch.from_numpy(x).cuda()[off:]
+    grid = g0 = -1
+    cta = True
+    if LAUNCH:
+        grid = int(rng.choice([0, 1, 2, 3, 7, 16, 37, 148, 296]))
+        g0 = int(rng.integers(-1, 5))
+        cta = bool(rng.integers(4))
+        nrmf._debug_set_grid(grid)
+        nrmf._debug_set_g0(g0)
+        nrmf._debug_set_cta_step(cta)
     r = nrmf.norm(xd, top=top).cpu().numpy()
+    if LAUNCH:
+        nrmf._debug_set_grid(0)
+        nrmf._debug_set_g0(-1)
+        nrmf._debug_set_cta_step(True)
     e = oracle.nrmf(x[off:], top=top)
     ok = np.asarray(r, dtype=dt).tobytes() == np.asarray(e, dtype=dt).tobytes()
     if not ok:
         bad += 1
-        print("MISMATCH", n, dt.__name__, dist, off, top, seed, flush=True)
+        print("MISMATCH", n, dt.__name__, dist, off, top, seed, grid, g0, cta, flush=True)
 print(f"{N} cases, {bad} mismatches")
 sys.exit(1 if bad else 0)
