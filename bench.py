@@ -214,13 +214,14 @@ def run_reference(args):
     sample = 1 << 24
     esz = np.dtype(dt).itemsize
     ts = []
-    for s in range(args.warmup + args.steps):
-        x = make_input(args.config, sample, (s * sample) % N_C3, dt)
-        t0 = time.perf_counter()
-        oracle.nrmf(x)
-        t1 = time.perf_counter()
-        if s >= args.warmup:
-            ts.append(t1 - t0)
+    with one_core() as core:
+        for s in range(args.warmup + args.steps):
+            x = make_input(args.config, sample, (s * sample) % N_C3, dt)
+            t0 = time.perf_counter()
+            oracle.nrmf(x)
+            t1 = time.perf_counter()
+            if s >= args.warmup:
+                ts.append(t1 - t0)
     ms = 1e3 * sum(ts) / len(ts)
     gbs = sample * esz / (ms * 1e-3) / 1e9
     line = {
@@ -230,11 +231,34 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32", "data": "synthetic",
         "config": {"workload": cfg_name(args.config), "n": N_C3, "sample_per_step": sample},
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"2^24 contiguous elements of the {args.config.upper()} array per step"},
+                         "sample": f"2^24 contiguous elements of the {args.config.upper()} array per step",
+                         "core": core, "nproc": os.cpu_count()},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+class one_core:
+    """Pin this process to one host core while the oracle is timed (SURVEY
+    §8(d): single-threaded oracle on one core); restores the old mask."""
+
+    def __enter__(self):
+        self.old = None
+        try:
+            self.old = os.sched_getaffinity(0)
+            core = max(self.old)
+            os.sched_setaffinity(0, {core})
+            return core
+        except (AttributeError, OSError):
+            return None
+
+    def __exit__(self, *a):
+        if self.old is not None:
+            try:
+                os.sched_setaffinity(0, self.old)
+            except OSError:
+                pass
 
 
 def cfg_name(c):
@@ -452,15 +476,16 @@ def run_ours(args):
         acc = {"relerr_eps": oracle.relerr(result, ex, dt), "ulp": ulp_distance(result, ex, dt),
                "exact_hex": np.asarray(ex, dtype=dt).tobytes()[::-1].hex(),
                "bound_thm3_eps": round(oracle.ub_relerr_H(12 + int(math.log2(max(1, n // 4096))), dt), 3)}
-        t0 = time.perf_counter()
-        o = oracle.nrmf(xh)
-        t_or = time.perf_counter() - t0
+        with one_core() as core:
+            t0 = time.perf_counter()
+            o = oracle.nrmf(xh)
+            t_or = time.perf_counter() - t0
         acc["bit_exact_vs_oracle"] = bool(np.asarray(o, dtype=dt).tobytes() == np.asarray(result, dtype=dt).tobytes())
         line["accuracy"] = acc
         line["cpu_baseline"] = {"value": round(total_bytes / t_or / 1e9, 4), "unit": "GB/s", "cores": 1,
                                 "kind": "oracle", "seconds": round(t_or, 3),
                                 "sample": f"full workload ({n} elements), single-threaded C oracle",
-                                "cpu": cpu_model()}
+                                "cpu": cpu_model(), "core": core, "nproc": os.cpu_count()}
         line["timing_s"] = {"gen": round(t_gen, 2), "exact": round(t_exact, 2), "oracle": round(t_or, 2)}
         # context: the same step right after the GPU idled through the CPU
         # oracle (not power-capped yet), 10 steps timed one by one; the line's
