@@ -22,7 +22,9 @@ def t(A, reps=20):
     return statistics.median(ts)
 
 
-for (r, c, ld, dt) in [(4096, 65536, 4096, torch.float64), (8192, 32768, 8192, torch.float64),
+for (r, c, ld, dt) in [(4096, 65536, 4096, torch.float64), (4096, 65536, 4160, torch.float64),
+                       (8192, 32768, 8192, torch.float64), (8192, 32768, 8256, torch.float64),
+                       (4096, 65536, 4160, torch.float32),
                        (4096, 65536, 4096, torch.float32), (4000, 65536, 4096, torch.float64),
                        (1000, 262144, 1000, torch.float64)]:
     B = torch.randn(c, ld, dtype=dt, device="cuda")
