@@ -475,6 +475,13 @@ def _debug_set_g0(g0: int):
     L.nrmf_debug_set_g0(g0)
 
 
+def _debug_set_gap_stream(on: bool):
+    """Test hook: gapped column blocks (ld > rows, rows % 4096 == 0) on the stream kernel (default on)."""
+    L = _load()
+    L.nrmf_debug_set_gap_stream.argtypes = [ctypes.c_int]
+    L.nrmf_debug_set_gap_stream(1 if on else 0)
+
+
 def _debug_set_cta_step(on: bool):
     """Test hook: the stream kernel's first combine step in shared memory (default on)."""
     L = _load()

@@ -383,7 +383,10 @@ static_assert(kWarps * WarpSmem<double>::kBytes + CtaSmem<double>::kBytes <= 227
 // single_tile).  Every consumed stage is refilled at once, so the slot to fill
 // is always the one just consumed.  State: 5 registers plus kernel-uniform
 // values.
-template <typename F>
+// GAP: column blocks with a gap between columns (ld > rows, rows a multiple
+// of T, 16-byte aligned columns): the walk also skips (ld - rows) elements at
+// every column end, and a new group's start is computed from its tile index.
+template <typename F, bool GAP = false>
 struct StreamLoader {
   static constexpr int BPI = 1;
   static constexpr bool kMaybePadding = false;
@@ -397,6 +400,22 @@ struct StreamLoader {
   int groups_left;       // further groups after it (-1: nothing left to load)
   int group_batches;     // G * J / kBatch            (kernel-uniform)
   int64_t skip_bytes;    // (W - 1) groups in bytes   (kernel-uniform)
+  // GAP only
+  int p_grp;             // group being loaded
+  int col_left;          // batches left in the current column
+  int grp_step;          // W                          (kernel-uniform)
+  int col_batches;       // tpc * J / kBatch           (kernel-uniform)
+  int64_t col_skip;      // (ld - rows) in bytes       (kernel-uniform)
+  int64_t tpc, ld;       // tiles per column, leading dimension (kernel-uniform)
+  const F* x;
+  int g0;                // (kernel-uniform)
+
+  __device__ __forceinline__ void seek(int grp) {
+    const int64_t tau = (int64_t)grp << g0;
+    const int64_t col = tau / tpc, tt = tau - col * tpc;
+    p_ptr = reinterpret_cast<const char*>(x + col * ld + tt * (int64_t)kTile);
+    col_left = (int)(tpc - tt) * (Cfg<F>::J / kBatch);
+  }
 
   __device__ __forceinline__ void issue(uint32_t slot) {
     if (groups_left < 0) return;
@@ -404,10 +423,19 @@ struct StreamLoader {
       bulk_load(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
                 policy_evict_first());
     p_ptr += kBatchBytes;
+    if (GAP && --col_left == 0) {
+      col_left = col_batches;
+      p_ptr += col_skip;
+    }
     if (--p_left == 0) {
       p_left = group_batches;
-      p_ptr += skip_bytes;
       --groups_left;
+      if (GAP) {
+        p_grp += grp_step;
+        if (groups_left >= 0) seek(p_grp);
+      } else {
+        p_ptr += skip_bytes;
+      }
     }
   }
   __device__ __forceinline__ void begin(int) {
@@ -560,7 +588,7 @@ __device__ __forceinline__ F single_tile(const TreeJob<F>& job, int64_t tau) {
   return warp_tile_exact<F, kPred>(tb, (int)remv);
 }
 
-template <typename F, bool TMA, int NT, bool STREAM>
+template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false>
 __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(const TreeJob<F> job) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr bool kPipe = TMA && NRMF_USE_TMA;
@@ -579,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   // a vector, or columns with ld == rows == a multiple of T)
   const int n_full = kStream ? (int)((job.ld == 0 ? job.len / kTile : job.n_items) >> job.g0) : 0;
 
-  StreamLoader<F> sl;
+  StreamLoader<F, GAP> sl;
   if (kStream) {
     using L = WarpSmem<F>;
     sl.my_s = smem_u32(smem) + w * L::kBytes;
@@ -593,8 +621,20 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     sl.p_left = sl.group_batches;
     // groups gw, gw + W, ... below n_full: this warp streams 1 + groups_left of them
     sl.groups_left = gw < n_full ? (int)((n_full - 1 - gw) / W) : -1;
-    sl.p_ptr = reinterpret_cast<const char*>(job.x + gw * G * (int64_t)kTile);
-    sl.skip_bytes = (W - 1) * G * (int64_t)kTile * (int64_t)sizeof(F);
+    if (GAP) {
+      sl.x = job.x;
+      sl.tpc = job.tpc;
+      sl.ld = job.ld;
+      sl.grp_step = W;
+      sl.col_batches = (int)job.tpc * (Cfg<F>::J / kBatch);
+      sl.col_skip = (job.ld - job.len) * (int64_t)sizeof(F);
+      sl.g0 = job.g0;
+      sl.p_grp = gw;
+      if (sl.groups_left >= 0) sl.seek(gw);
+    } else {
+      sl.p_ptr = reinterpret_cast<const char*>(job.x + gw * G * (int64_t)kTile);
+      sl.skip_bytes = (W - 1) * G * (int64_t)kTile * (int64_t)sizeof(F);
+    }
     for (int st = 0; st < kStages; ++st) sl.issue(st);
   }
   const uint32_t cta_s = smem_u32(smem) + kWarps * WarpSmem<F>::kBytes;
@@ -655,7 +695,12 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         // group levels as a shuffle tree (contiguous pairs, the same tree)
         const uint32_t xs = sl.my_s + WarpSmem<F>::kXs;
         for (int k = 0; k < G; ++k) {  // rolled
-          const F tv = warp_tile_exact<F, kVec>(job.x + (grp * G + k) * (int64_t)kTile, kTile);
+          const F* tb = job.x + (grp * G + k) * (int64_t)kTile;  // contiguous tiles
+          if (GAP) {
+            int64_t remv;
+            tile_at(job, grp * G + k, tb, remv);  // a full tile of a gapped column block
+          }
+          const F tv = warp_tile_exact<F, kVec>(tb, kTile);
           if (lane == 0) {
             st_shared(xs + k * (uint32_t)sizeof(F), tv);
             if (job.tile_out != nullptr) job.tile_out[grp * G + k] = tv;
@@ -1003,16 +1048,17 @@ static size_t kernel_smem() {
   return (size_t)kWarps * kStages * kBatchBytes + (size_t)kWarps * kStages * 8;
 }
 
-template <typename F, bool TMA, int NT, bool STREAM>
+template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false>
 static int blocks_per_sm() {
   static int cached = 0;
   if (cached == 0) {
     const size_t sm = kernel_smem<F, TMA, STREAM>();
     if (sm > 48 * 1024)
-      cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM, GAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sm);
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM>, kThreads, sm) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM, GAP>, kThreads,
+                                                      sm) !=
             cudaSuccess ||
         b < 1)
       b = 1;
@@ -1024,6 +1070,7 @@ static int blocks_per_sm() {
 static int g_grid_override = 0;  // test hook: force a grid size (0 = automatic)
 static int g_g0_override = -1;   // dev hook: force the warp-group level count g0 (-1 = automatic)
 static int g_cta_step0 = NRMF_CTA_STEP;  // dev hook: first combine step in shared memory (stream kernel)
+static int g_gap_stream = 1;     // test hook: gapped column blocks on the stream kernel (0: general kernel)
 
 // Launch the tree kernel over items (tiles) with mapping (tpc, ld, len).
 template <typename F>
@@ -1035,7 +1082,11 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   // contiguous tiles (a vector, or whole columns of T-multiple length stored
   // back to back): warp groups are contiguous, the pointer-walk producer applies
   const bool stream = vec && (ld == 0 || (ld == len && len % kTile == 0));
-  int64_t grid = (int64_t)device_sms() * (stream ? blocks_per_sm<F, true, 1, true>()
+  // column blocks with gaps (ld > rows, rows a multiple of T; vec implies
+  // 16-byte aligned columns): the stream kernel with the gap-skipping walk
+  const bool gap = vec && g_gap_stream && ld > len && len % kTile == 0;
+  int64_t grid = (int64_t)device_sms() * (gap      ? blocks_per_sm<F, true, 1, true, true>()
+                                          : stream ? blocks_per_sm<F, true, 1, true>()
                                           : vec  ? blocks_per_sm<F, true, NRMF_NT, false>()
                                                  : blocks_per_sm<F, false, 1, false>());
   if (g_grid_override > 0) grid = g_grid_override;
@@ -1074,7 +1125,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   int g0_max = 0;
   // groups of up to kMaxGroup tiles on the stream kernel, 8 elsewhere
   // (the column kernel's counter merge has three levels)
-  const int gmax = stream ? (sizeof(F) == 4 ? 4 : 3) : 3;
+  const int gmax = (stream || gap) ? (sizeof(F) == 4 ? 4 : 3) : 3;
   {
     const int64_t W = grid * kWarps;
     double best = 0.0;
@@ -1095,7 +1146,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   Plan pl = combine ? make_plan(n_items, p2, g0_max)
                     : make_plan(n_items, int64_t(1) << g0_max, g0_max);
   bool cta_step0 = false;
-  if (stream && combine && kWarps == 16 && g_cta_step0 &&
+  if ((stream || gap) && combine && kWarps == 16 && g_cta_step0 &&
       ((n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0) >= grid * kWarps) {
     const Plan p4 = make_plan(n_items, p2, g0_max, 4);
     if (p4.nsteps >= 1 && p4.lg_fan[0] == 4 && p4.g0 == pl.g0) {
@@ -1116,7 +1167,9 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   job.cta_minor = n_groups < grid * kWarps;
   job.cta_step0 = cta_step0 ? 1 : 0;
   grid = std::min<int64_t>(grid, n_groups);
-  if (stream) {
+  if (gap) {
+    nrmf_tree_kernel<F, true, 1, true, true><<<(unsigned)grid, kThreads, kernel_smem<F, true, true>(), s>>>(job);
+  } else if (stream) {
     nrmf_tree_kernel<F, true, 1, true><<<(unsigned)grid, kThreads, kernel_smem<F, true, true>(), s>>>(job);
   } else if (vec && pl.g0 >= 1 && NRMF_NT == 2) {
     blocks_per_sm<F, true, NRMF_NT, false>();
@@ -1466,6 +1519,11 @@ int nrmf_debug_set_trace(void* buf, unsigned cap) {
 
 int nrmf_debug_set_g0(int g0) {
   g_g0_override = (g0 < 0 || g0 > 4) ? -1 : g0;
+  return NRMF_OK;
+}
+
+int nrmf_debug_set_gap_stream(int on) {
+  g_gap_stream = on != 0;
   return NRMF_OK;
 }
 

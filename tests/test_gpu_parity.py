@@ -214,6 +214,34 @@ def test_cta_combine_step_columns(nrmf, dt, rows):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("rows,cols,gap", [(T, 6000, 64), (3 * T, 2001, 64), (2 * T, 3500, 4096 + 32),
+                                           (5 * T, 1300, 16)])
+@pytest.mark.parametrize("grid", [0, 2, 37])
+def test_cols_gapped_stream(nrmf, dt, rows, cols, gap, grid):
+    """Column blocks with a gap between columns (ld = rows + gap, rows a
+    multiple of T; ld 16-byte aligned for both precisions): the stream
+    kernel's walk skips the gaps and seeks every new group from its tile
+    index (tiles per column 1, 2, 3, 5 -- groups span columns when tpc < G).
+    Column norms and frob equal the oracle's, with the gapped stream path and
+    with the general kernel."""
+    ld = rows + gap
+    A = gen.colscaled_normal(rows + cols, rows, cols, ld=ld, dtype=dt)
+    A.reshape(cols, ld)[:, rows:] = np.nan                # the gaps must never be read
+    At = dev(A).as_strided((rows, cols), (1, ld))
+    ecol, efr = oracle.cols(A, rows, cols, ld)
+    try:
+        nrmf._debug_set_grid(grid)
+        for on in (True, False):
+            nrmf._debug_set_gap_stream(on)
+            col, fr = nrmf.cols(At)
+            assert col.cpu().numpy().tobytes() == ecol.tobytes(), on
+            assert bits(fr.cpu().numpy(), dt) == bits(efr, dt), on
+    finally:
+        nrmf._debug_set_gap_stream(True)
+        nrmf._debug_set_grid(0)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_special_values(nrmf, dt):
     """Non-finite inputs follow Listing 2 literally on both sides (reading R4):
     inf anywhere -> inf; a NaN collapses to +0 when it meets a +0 leaf."""
