@@ -1116,12 +1116,14 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   // Warp-group size G = 2^g0 (<= 8 tiles; 16 for fp32 on the stream kernel).
   // The persistent warps take groups round-robin, so the makespan is
   // ceil(groups / W) groups of G tiles, and a group costs about G + c tiles
-  // (its cross-thread tail and announce: c = 1/3 tile, fitted to forced-g0
-  // timings at n = 2^26..2^30 with cool-downs, tools/g0_sweep.py; fp32 was
-  // 4/3 before the CTA combine step made the announce cheap: fp32 2^28 now
-  // runs G = 4, 190 -> 180 us).  Take the G minimising ceil(groups / W) *
-  // (G + c), the larger on ties.  The tree does not depend on g0.
-  constexpr double kGroupCost = 1.0 / 3.0;
+  // (its cross-thread tail and announce).  c = 1/12 tile, fitted to forced-g0
+  // timings at n = 2^22..2^30 (tools/g0_sweep.py --both --lg=...): it was 1/3
+  // (4/3 for fp32) before the CTA combine step made the announce cheap; with
+  // 1/12 fp64 2^26 runs G = 1 (132 -> 123 us) and fp32 2^27 G = 2 (100 ->
+  // 94 us), the other sizes keep their G.  Take the G minimising
+  // ceil(groups / W) * (G + c), the larger on ties.  The tree does not depend
+  // on g0.
+  constexpr double kGroupCost = 1.0 / 12.0;
   int g0_max = 0;
   // groups of up to kMaxGroup tiles on the stream kernel, 8 elsewhere
   // (the column kernel's counter merge has three levels)

@@ -33,7 +33,7 @@ def t(x, reps):
 
 
 for dt in (torch.float64, torch.float32):
-    for lg in (12, 16, 18, 20, 22, 24, 26, 28, 30):
+    for lg in (12, 16, 18, 20, 22, 23, 24, 25, 26, 27, 28, 29, 30):
         x = torch.randn(1 << lg, dtype=dt, device="cuda")
         ms = t(x, 20 if lg >= 28 else 50)
         print(f"{str(dt):14s} n=2^{lg:2d}: {ms*1e3:9.1f} us  {x.numel()*x.element_size()/ms/1e6:8.1f} GB/s", flush=True)
