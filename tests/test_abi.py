@@ -1,6 +1,5 @@
 """The C-ABI library loads and exports every symbol include/nrmf.h declares;
 host-only entry points (no GPU needed) behave as documented."""
-import ctypes
 import os
 import re
 

@@ -356,7 +356,6 @@ def test_dist_world1(nrmf):
 def test_workspace_contents_do_not_matter(nrmf):
     """A workspace full of garbage (0xFF), and one reused across calls of
     different shapes and functions, gives the same bits."""
-    import ctypes
     L = nrmf.lib()
     x = gen.normal(4, 300 * T + 7)
     xd = dev(x)

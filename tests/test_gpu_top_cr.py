@@ -3,7 +3,6 @@ level.  GPU cr_hypot is checked against the oracle's exact cr_hypot (exact
 integer RN(sqrt(x^2+y^2))), and every entry point with top="cr" against the
 oracle's tree with cr_hypot above the tiles, bit for bit."""
 import ctypes
-import math
 import os
 import subprocess
 
