@@ -493,6 +493,11 @@ __device__ __forceinline__ unsigned ld_volatile_shared_u32(uint32_t a) {
   asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_acquire_cta_shared_u32(uint32_t a) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_shared_u32(uint32_t a, unsigned v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -563,7 +568,10 @@ __device__ __forceinline__ void cta_arrive(const TreeJob<F>& job, uint32_t cta_s
   const uint32_t slot = (uint32_t)r & (kCtaSlots - 1);
   if (lane == 0) {
     const uint32_t ts = cta_s + C::kTag + slot * 4;
-    while (ld_volatile_shared_u32(ts) != (unsigned)r) __nanosleep(64);  // slot still serves round r - kCtaSlots
+    // slot still serves round r - kCtaSlots until its claimer frees it; the
+    // acquire orders this round's value store and count after the claimer's
+    // reads and counter reset
+    while (ld_acquire_cta_shared_u32(ts) != (unsigned)r) __nanosleep(64);
     st_shared(cta_s + C::kVals + (slot * 16 + (grp & 15)) * (uint32_t)sizeof(F), gv);
     red_add_release_cta_shared(cta_s + C::kCnt + slot * 4, 1u);
   }
