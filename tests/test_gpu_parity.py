@@ -242,6 +242,27 @@ def test_cols_gapped_stream(nrmf, dt, rows, cols, gap, grid):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("groups_lg", [7, 8])
+@pytest.mark.parametrize("case", ["normal", "nan", "huge", "zero_run", "cr"])
+def test_split_kernel_wide_last_step(nrmf, dt, groups_lg, case):
+    """Small calls (split kernel) finish with one climb of up to 8 levels
+    (fan-in 128 / 256): its fast path, and its exact fallback (a NaN tile, an
+    out-of-fast-domain tile value, +0 tiles, the cr top), against the oracle."""
+    G = 1 if dt == np.float64 else 2                       # split-kernel tiles per group
+    n = (1 << groups_lg) * G * T - 3 * T // 2             # ragged last tile
+    xh = gen.normal(groups_lg * 10 + len(case), n, dtype=dt)
+    if case == "nan":
+        xh[5 * T + 7] = np.nan
+    elif case == "huge":
+        xh[9 * T: 10 * T] *= dt(2.0 ** 1010) if dt == np.float64 else dt(2.0 ** 110)
+    elif case == "zero_run":
+        xh[: 40 * T] = 0
+    top = "cr" if case == "cr" else "v1"
+    exp = bits(oracle.nrmf(xh, top=top), dt)
+    assert bits(nrmf.norm(dev(xh), top=top).cpu().numpy(), dt) == exp
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_special_values(nrmf, dt):
     """Non-finite inputs follow Listing 2 literally on both sides (reading R4):
     inf anywhere -> inf; a NaN collapses to +0 when it meets a +0 leaf."""
