@@ -695,9 +695,16 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         st_shared(sl.my_s + WarpSmem<F>::kXs + (k * 32 + lane) * (uint32_t)sizeof(F), c);
       }
       __syncwarp();
+#ifdef NRMF_PROBE_NO_GROUPCROSS  // dev-only timing probe: no cross-thread/group levels (wrong results)
+      if (!__any_sync(0xffffffffu, node.bad)) {
+        ld_shared(sl.my_s + WarpSmem<F>::kXs + lane * (uint32_t)sizeof(F), gv[0]);
+        group_done = true;
+      }
+#else
       if (!__any_sync(0xffffffffu, node.bad))
         group_done = group_cross<F>(node, sl.my_s + WarpSmem<F>::kXs, G, job.top_cr, gv[0],
                                     job.tile_out != nullptr ? job.tile_out + grp * G : nullptr);
+#endif
       if (!group_done) {
         // exact path: the G tile values through the xs area, then the lg G
         // group levels as a shuffle tree (contiguous pairs, the same tree)
