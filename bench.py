@@ -279,12 +279,16 @@ def run_ours(args):
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
+    # the distributed step (shard, tree kernel, NCCL allgather, rank tree) for
+    # N > 1; NRMF_BENCH_DIST=1 runs it on a 1-rank group (under torchrun) to
+    # exercise that path on one GPU
+    dist = world > 1 or os.environ.get("NRMF_BENCH_DIST", "0") == "1"
     local = env_int("LOCAL_RANK", 0)
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:
+    if dist:
         td.init_process_group("nccl", device_id=device)
 
     config = args.config
@@ -292,7 +296,7 @@ def run_ours(args):
     tdt = torch.float64 if dt == np.float64 else torch.float32
     esz = np.dtype(dt).itemsize
     n = N_C3 if config in ("c3", "c2") else (1 << 20)
-    off, cnt = nrmf.shard(n, world, rank) if world > 1 else (0, n)
+    off, cnt = nrmf.shard(n, world, rank) if dist else (0, n)
 
     t0 = time.time()
     x_host = torch.empty(cnt, dtype=tdt).pin_memory()
@@ -310,11 +314,11 @@ def run_ours(args):
 
     stream = torch.cuda.current_stream(device)
     out = torch.empty((), dtype=tdt, device=device)
-    comm = nrmf.comm_for(None) if world > 1 else None
+    comm = nrmf.comm_for(None) if dist else None
 
-    p2p = world > 1 and os.environ.get("NRMF_BENCH_P2P", "0") == "1"
+    p2p = dist and os.environ.get("NRMF_BENCH_P2P", "0") == "1"
     pgroup = nrmf.P2PGroup() if p2p else None
-    if world > 1:
+    if dist:
         # one CUDA graph per step: counter memset, tile-tree kernel, and either
         # ncclAllGather of one scalar + rank-tree kernel, or with
         # NRMF_BENCH_P2P=1 the peer-memory exchange kernel (opt-in:
@@ -347,14 +351,14 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist:
         td.barrier()
     # inputs below 4x the 126 MB L2 (C1: 8 MiB): flush L2 before every timed step
     small = cnt * esz < 4 * 126 * 2**20
     flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=device) if small else None
     with ClockSampler(local) as clk:
         ms = time_loop(step, args.steps, stream, flush)
-    if world > 1:
+    if dist:
         tt = torch.tensor([ms], dtype=torch.float64, device=device)
         td.all_reduce(tt, op=td.ReduceOp.MAX)
         ms = tt.item()
@@ -364,7 +368,7 @@ def run_ours(args):
     # dominant kernel alone (the local tile-tree kernel), same stream, same data;
     # and the 8-byte allgather alone (torch's NCCL, same ranks)
     allgather_us = None
-    if world > 1:
+    if dist:
         kern_ms = time_loop(lambda: nrmf.norm(x, out=out), args.steps, stream)
         one = torch.zeros(1, dtype=tdt, device=device)
         allv = torch.zeros(world, dtype=tdt, device=device)
@@ -398,7 +402,7 @@ def run_ours(args):
                    "tree_version": nrmf.tree_version(), "seed": 1},
         "gpu_launches": launches_per_step * args.steps,
         "graph": graph is not None,
-        "rank_exchange": ("p2p" if p2p else "nccl_allgather") if world > 1 else None,
+        "rank_exchange": ("p2p" if p2p else "nccl_allgather") if dist else None,
         "clocks": clocks,
         "elements_per_s": round(n / (ms * 1e-3), 1),
         "roofline": {"bound": "hbm", "achieved": round(kern_gbs, 2), "peak": hbm_peak, "unit": "GB/s",
@@ -424,7 +428,7 @@ def run_ours(args):
 
     # ---------------- e2e: host-resident input through the public API
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    if world == 1:
+    if not dist:
         host_out = torch.empty((), dtype=tdt).pin_memory()
 
         def e2e_step():
@@ -463,7 +467,7 @@ def run_ours(args):
     line["e2e"] = {"value": round(total_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                    "h2d_bytes_per_step": total_bytes, "d2h_bytes_per_step": esz,
                    "ms_per_step": round(e2e_ms, 3), "steps": e2e_steps, "same_bits": bool(e2e_ok),
-                   "api": "nrmf.norm(pinned host tensor) -> nrmf_host_d" if world == 1 else
+                   "api": "nrmf.norm(pinned host tensor) -> nrmf_host_d" if not dist else
                           "pinned H2D copy + nrmf.dist -> nrmf_dist_d"}
 
     # ---------------- extras (rank 0, N=1): accuracy, oracle CPU baseline, SNRMF point
@@ -500,7 +504,7 @@ def run_ours(args):
             line["other_configs"] = other_configs(nrmf, device, stream, hbm_peak)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist:
         if pgroup is not None:
             pgroup.close()
         comm.close()

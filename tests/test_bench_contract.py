@@ -69,3 +69,43 @@ def test_gpu_arm_prints_one_contract_line():
     assert d["accuracy"]["bit_exact_vs_oracle"]
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p2p", ["0", "1"])
+def test_gpu_arm_distributed_step_on_one_rank(p2p):
+    """The N > 1 step (shard, tree kernel, NCCL allgather or the P2P
+    exchange, rank tree; one CUDA graph) run on a 1-rank group under torchrun
+    (NRMF_BENCH_DIST=1): the line is produced, the graph captured, e2e bits
+    equal the device bits, and the result equals the single-GPU tree's."""
+    env = dict(os.environ, NRMF_BENCH_DIST="1", NRMF_BENCH_P2P=p2p)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    port = str(29650 + int(p2p))
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", port, os.path.join(ROOT, "bench.py"),
+                        "--gpus", "1", "--steps", "3", "--warmup", "3", "--no-extras", "--e2e-steps", "1"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["rank_exchange"] == ("p2p" if p2p == "1" else "nccl_allgather")
+    assert d["graph"] and d["e2e"]["same_bits"] and d["allgather_8B_us"] > 0
+    assert d["result_hex"] == _c3_oracle_hex()
+
+
+_C3_HEX = []
+
+
+def _c3_oracle_hex():
+    """The oracle's value of bench.py's C3 workload (n = 2^30 N(0,1), seed 1),
+    big-endian hex as bench.py prints it (computed once, ~15 s on one core)."""
+    if not _C3_HEX:
+        import numpy as np
+
+        import nrmf_inputs as gen
+        import oracle
+        x = gen.normal(1, 1 << 30, 0, dtype=np.float64)
+        _C3_HEX.append(np.asarray(oracle.nrmf(x), dtype=np.float64).tobytes()[::-1].hex())
+    return _C3_HEX[0]
