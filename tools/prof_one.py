@@ -1,6 +1,6 @@
 """Dev tool: a short nrmf_d / nrmf_s run of one libnrmf.so variant, for ncu.
 
-    python tools/prof_one.py lib.so [d|s] [reps]"""
+    python tools/prof_one.py lib.so [d|s] [reps] [lg_n]"""
 import sys
 
 import torch
@@ -11,7 +11,7 @@ from bench_variants import load  # noqa: E402
 L = load(sys.argv[1])
 dt = torch.float64 if (sys.argv[2] if len(sys.argv) > 2 else "d") == "d" else torch.float32
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-n = 1 << 30
+n = 1 << (int(sys.argv[4]) if len(sys.argv) > 4 else 30)
 x = torch.randn(n, dtype=dt, device="cuda")
 ws = torch.zeros(L.nrmf_workspace_bytes(n, x.element_size()), dtype=torch.uint8, device="cuda")
 out = torch.empty((), dtype=dt, device="cuda")
