@@ -25,8 +25,12 @@ Functions (and what pins each, independently of this package)
   cols_shard_frobs                   subtrees -- == the global frob for G = 1..8
   exact(x)                           exactly rounded RN(sqrt(sum x^2))
                                      -- Python Fraction + isqrt, closed forms
-  relerr(r, ref, dtype)              e:relerr (P:737-743)
-  ub_relerr_H(depth, dtype)          Thm 3 + e:reH bound -- Table 3
+  relerr(r, ref, dtype)              e:relerr -- results one/two float
+                                     spacings from powers of two (numpy's finfo
+                                     eps), operand order, binade invariance
+  ub_relerr_H(depth, dtype)          Thm 3 + e:reH bound -- Table 3 at
+                                     eps_D; a hand-worked second-order Taylor
+                                     expansion at eps_S and eps_D
   bounds.py                          Thm 1-3 recurrences -- all 90 Table 3 values
 
 Parity unpinned: the absolute result values on random data -- the paper
