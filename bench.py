@@ -173,6 +173,49 @@ def burst_point(step, stream, total_bytes, hbm_peak, local, flush=None):
             "note": "after ~15 s idle (CPU oracle); context only, not the line's value"}
 
 
+def sustained_point(step, stream, total_bytes, hbm_peak, local, flush=None, launches=300):
+    """Context: the step launched `launches` times back to back
+    right after the burst point, each launch timed by its own events; the
+    median of the last 100 is the power-capped steady state.  Energy per call
+    from the NVML total-energy counter over all launches."""
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(launches)]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for e0, e1 in evs:
+            if flush is not None:
+                flush.zero_()
+            e0.record(stream)
+            step()
+            e1.record(stream)
+        torch.cuda.synchronize()
+    ts = [a.elapsed_time(b) for a, b in evs]
+    last = statistics.median(ts[-100:])
+    first = statistics.median(ts[:50])
+    clocks = clk.summary()
+    d = {"launches": launches, "first50_median_ms": round(first, 4), "last100_median_ms": round(last, 4),
+         "value": round(total_bytes / (last * 1e-3) / 1e9, 2), "unit": "GB/s",
+         "frac_hbm": round(total_bytes / (last * 1e-3) / 1e9 / hbm_peak, 4), "clocks": clocks}
+    if getattr(clk, "e1", None) is not None and flush is None:
+        d["energy_j_per_call"] = round((clk.e1 - clk.e0) * 1e-3 / launches, 3)
+        d["avg_power_w"] = round((clk.e1 - clk.e0) * 1e-3 / (sum(ts) * 1e-3), 1)
+    return d
+
+
+def golden_hex(config):
+    """The oracle's value of this workload (tests/golden/oracle_bench_values.txt)."""
+    p = os.path.join(ROOT, "tests", "golden", "oracle_bench_values.txt")
+    try:
+        with open(p) as f:
+            for ln in f:
+                parts = ln.split()
+                if len(parts) == 5 and parts[0] == config:
+                    return parts[3]
+    except OSError:
+        pass
+    return None
+
+
 def time_loop(fn, steps: int, stream, flush=None):
     import torch
     if flush is not None:
@@ -316,18 +359,27 @@ def run_ours(args):
     out = torch.empty((), dtype=tdt, device=device)
     comm = nrmf.comm_for(None) if dist else None
 
-    p2p = dist and os.environ.get("NRMF_BENCH_P2P", "0") == "1"
-    pgroup = nrmf.P2PGroup() if p2p else None
+    # rank exchange of the N > 1 step: the peer-memory exchange fused into the
+    # tree kernel (nrmf_dist_p2p_d; default) or NCCL
+    # (NRMF_BENCH_P2P=0: ncclAllGather of one scalar + the rank-tree kernel);
+    # if the peer buffers cannot be mapped, NCCL, and the line says so
+    p2p = dist and os.environ.get("NRMF_BENCH_P2P", "1") == "1"
+    pgroup, p2p_note = None, None
+    if p2p:
+        try:
+            pgroup = nrmf.P2PGroup()      # raises on every rank if any rank cannot map a peer
+        except Exception as e:  # noqa: BLE001
+            p2p, p2p_note = False, f"P2P setup failed ({e}); NCCL exchange"
     if dist:
-        # one CUDA graph per step: counter memset, tile-tree kernel, and either
-        # ncclAllGather of one scalar + rank-tree kernel, or with
-        # NRMF_BENCH_P2P=1 the peer-memory exchange kernel (opt-in:
-        # validated by emulated ranks on one GPU, not yet on several)
+        # one CUDA graph per step: counter memset + tile-tree kernel with the
+        # peer exchange at its root (p2p), or counter memset, tile-tree kernel,
+        # ncclAllGather of one scalar and the rank-tree kernel
         if p2p:
             call = lambda: nrmf.dist_p2p(x, n, pgroup, out=out)  # noqa: E731
+            launches_per_step = 1  # the tile-tree kernel (exchange and rank tree inside)
         else:
             call = lambda: nrmf.dist(x, n, comm=comm, out=out)  # noqa: E731
-        launches_per_step = 2  # tile-tree kernel + rank-tree kernel (the NCCL allgather is NCCL's)
+            launches_per_step = 2  # tile-tree kernel + rank-tree kernel (the NCCL allgather is NCCL's)
     else:
         # the step (counter memset + tree kernel) replayed from a CUDA graph:
         # device time without the Python/ctypes launch overhead (matters at C1)
@@ -358,12 +410,24 @@ def run_ours(args):
     flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=device) if small else None
     with ClockSampler(local) as clk:
         ms = time_loop(step, args.steps, stream, flush)
+    per_rank_ms = [ms]
     if dist:
         tt = torch.tensor([ms], dtype=torch.float64, device=device)
-        td.all_reduce(tt, op=td.ReduceOp.MAX)
-        ms = tt.item()
+        allt = torch.zeros(world, dtype=torch.float64, device=device)
+        td.all_gather_into_tensor(allt, tt)
+        per_rank_ms = [round(v, 4) for v in allt.tolist()]
+        ms = max(allt.tolist())
         td.barrier()
     result = out.cpu().item()
+    result_hex = np.asarray(result, dtype=dt).tobytes()[::-1].hex()
+    if dist:
+        # every rank must hold the same bits
+        hx = torch.tensor([int(result_hex, 16)], dtype=torch.int64, device=device)
+        allh = torch.zeros(world, dtype=torch.int64, device=device)
+        td.all_gather_into_tensor(allh, hx)
+        ranks_agree = len(set(allh.tolist())) == 1
+    else:
+        ranks_agree = True
 
     # dominant kernel alone (the local tile-tree kernel), same stream, same data;
     # and the 8-byte allgather alone (torch's NCCL, same ranks)
@@ -420,11 +484,18 @@ def run_ours(args):
                                "steps): coarse, +-15 %; tools/energy.py measures over 300 launches")
     if allgather_us is not None:
         line["allgather_8B_us"] = allgather_us
+    if p2p_note:
+        line["rank_exchange_note"] = p2p_note
     tr = load_traffic(esz)
     if tr is not None:
         line["roofline"]["traffic"] = tr
-    if rank == 0:
-        line["result_hex"] = np.asarray(result, dtype=dt).tobytes()[::-1].hex()
+    line["per_rank_ms"] = per_rank_ms
+    line["result_hex"] = result_hex
+    line["ranks_same_bits"] = ranks_agree
+    # the N = 1 tree's bits: the oracle's value of this workload (golden file
+    # written by tools/make_golden_bench.py from oracle/ only)
+    want = golden_hex(config)
+    line["same_bits_as_1gpu_tree"] = (result_hex == want) if want is not None else None
 
     # ---------------- e2e: host-resident input through the public API
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -449,7 +520,10 @@ def run_ours(args):
 
         def e2e_step():
             xdev.copy_(x_host, non_blocking=True)
-            nrmf.dist(xdev, n, comm=comm, out=out)
+            if p2p:
+                nrmf.dist_p2p(xdev, n, pgroup, out=out)
+            else:
+                nrmf.dist(xdev, n, comm=comm, out=out)
             return out.cpu()
         e2e_step()
         td.barrier()
@@ -463,12 +537,14 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
         td.all_reduce(tt, op=td.ReduceOp.MAX)
         e2e_ms = tt.item()
-        e2e_ok = out.cpu().item() == result
+        v = out.cpu().item()
+        e2e_ok = v == result or (math.isnan(result) and math.isnan(v))
     line["e2e"] = {"value": round(total_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                    "h2d_bytes_per_step": total_bytes, "d2h_bytes_per_step": esz,
                    "ms_per_step": round(e2e_ms, 3), "steps": e2e_steps, "same_bits": bool(e2e_ok),
                    "api": "nrmf.norm(pinned host tensor) -> nrmf_host_d" if not dist else
-                          "pinned H2D copy + nrmf.dist -> nrmf_dist_d"}
+                          ("pinned H2D copy + nrmf.dist_p2p -> nrmf_dist_p2p_d" if p2p else
+                           "pinned H2D copy + nrmf.dist -> nrmf_dist_d")}
 
     # ---------------- extras (rank 0, N=1): accuracy, oracle CPU baseline, SNRMF point
     if rank == 0 and world == 1 and not args.no_extras:
@@ -495,6 +571,7 @@ def run_ours(args):
         # oracle (not power-capped yet), 10 steps timed one by one; the line's
         # value stays the sustained K-step number above
         line["burst"] = burst_point(step, stream, total_bytes, hbm_peak, local, flush)
+        line["sustained"] = sustained_point(step, stream, total_bytes, hbm_peak, local, flush)
         line["context_sumsq"] = sumsq_context(x, ex, dt, ms, args, stream)
         if config == "c3" and not args.no_snrmf:
             line["snrmf"] = snrmf_point(nrmf, device, stream, args, hbm_peak)
@@ -688,12 +765,42 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-snrmf", action="store_true")
     ap.add_argument("--no-other", action="store_true", help="skip the C2/C4/C5 report (other_configs)")
+    ap.add_argument("--launcher", default="auto", choices=["auto", "torchrun"],
+                    help="torchrun: re-exec under torch.distributed.run even for --gpus 1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and (args.gpus > 1 or args.launcher == "torchrun"):
+        return reexec_torchrun(args)
+    world = env_int("WORLD_SIZE", 1)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     return run_ours(args)
+
+
+def reexec_torchrun(args):
+    """--gpus N without a torchrun environment: run this script under
+    torch.distributed.run with N ranks (one per GPU), as the driver would."""
+    import socket
+    import subprocess
+    try:
+        import torch
+        have = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        have = 0
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, {have} visible", file=sys.stderr)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    argv = [a for a in sys.argv[1:]]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

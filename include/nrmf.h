@@ -31,7 +31,8 @@
  *    Every call is asynchronous and ordered on stream; the library never
  *    synchronizes the device, never allocates device memory and never prints.
  *  - ws is a caller-owned device workspace of at least the size returned by the
- *    matching *_workspace_bytes call.  Its contents on entry do not matter
+ *    matching *_workspace_bytes call, 16-byte aligned (cudaMalloc and torch
+ *    allocations are; NRMF_EALIGN otherwise).  Its contents on entry do not matter
  *    (the call clears the few bytes of arrival counters it uses, on stream,
  *    before its kernel).  A workspace must not be shared by calls that may
  *    run concurrently (distinct workspaces and streams make the calls
@@ -162,6 +163,28 @@ int nrmf_dist_ex_d(int64_t n_global, int64_t offset, int64_t count, const double
 int nrmf_dist_ex_s(int64_t n_global, int64_t offset, int64_t count, const float *x_local,
                    float *out, int flags, void *ws, size_t ws_bytes, void *nccl_comm, void *stream);
 
+/* The two halves of nrmf_dist_[ds], for callers that move the rank values  */
+/* themselves (their own collective, MPI, ...) -- and the kernels the NCCL    */
+/* and peer-memory paths run:                                                 */
+/*  nrmf_dist_local_[ds]: *local_out (device, 1 element) = the value of this  */
+/*    rank's aligned subtree (the same tree kernel as nrmf_[ds]; +0 for a     */
+/*    rank that owns no data); arguments and workspace as nrmf_dist_[ds],     */
+/*    with world/rank given explicitly.                                       */
+/*  nrmf_rank_combine_[ds]: *out = the rank tree (the top lg min(world, P2)   */
+/*    levels of the global tree) over values[0 .. min(world, P2)) (device, in  */
+/*    rank order; P2 = pow2 >= ceil(n_global/T)).  One CTA, no workspace.      */
+/* Gathering every rank's local_out in rank order and combining them gives    */
+/* bitwise nrmf_[ds] of the whole array (tested through these two calls for   */
+/* 2, 4 and 8 ranks on one GPU).                                             */
+int nrmf_dist_local_d(int64_t n_global, int world, int rank, int64_t offset, int64_t count,
+                      const double *x_local, double *local_out, int flags, void *ws, size_t ws_bytes,
+                      void *stream);
+int nrmf_dist_local_s(int64_t n_global, int world, int rank, int64_t offset, int64_t count,
+                      const float *x_local, float *local_out, int flags, void *ws, size_t ws_bytes,
+                      void *stream);
+int nrmf_rank_combine_d(int64_t n_global, int world, const double *values, double *out, int flags, void *stream);
+int nrmf_rank_combine_s(int64_t n_global, int world, const float *values, float *out, int flags, void *stream);
+
 /* ------------------------------------------------------------------------ */
 /* Column norms of a column-major rows x cols_global matrix whose columns are */
 /* sharded in blocks over the ranks.  Canonical block: P2c = pow2 */
@@ -188,10 +211,14 @@ int nrmf_cols_dist_s(int64_t rows, int64_t cols_global, int64_t ld, int64_t col_
 
 /* ------------------------------------------------------------------------ */
 /* The rank level through peer memory instead of NCCL: the same  */
-/* canonical shards and the same rank tree as nrmf_dist_[ds], but the rank    */
-/* values are exchanged by one warp per rank with P2P stores into every       */
-/* peer's buffer (CUDA IPC over NVLink) and a flag, then each rank evaluates   */
-/* the rank tree -- one tiny kernel instead of ncclAllGather + a kernel.       */
+/* canonical shards and the same rank tree as nrmf_dist_[ds], but the        */
+/* exchange is fused into the tree kernel: the warp that evaluates the rank's */
+/* subtree root stores it into every peer's buffer (P2P stores to CUDA-IPC-    */
+/* mapped memory over NVLink) with a release flag, waits for every rank's      */
+/* value in its own buffer, evaluates the rank tree and writes *out -- one     */
+/* kernel per call, no ncclAllGather and no rank-tree launch (P:1077-1084:     */
+/* contiguous chunks per worker, combined in a fixed order).  The wait runs    */
+/* only after this rank's whole subtree is done (ranks are distinct GPUs).     */
 /* Setup (once per rank, collective through the caller's own channel):        */
 /*   nrmf_p2p_alloc(&buf) -- nrmf_p2p_buffer_bytes() of device memory,       */
 /*     zero-filled (the one allocation the library makes; free it with     */

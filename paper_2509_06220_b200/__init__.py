@@ -11,6 +11,8 @@ missing or a call fails, an exception is raised.
     norm_complex(z)         ||z||_F of a complex64/complex128 tensor
     cols(A)                 (column norms, Frobenius norm) of a column-major matrix
     dist(x_local, n_global) ||x||_F of an array sharded over torch.distributed ranks
+    dist_p2p(x_local, n_global, pg)  the same, rank exchange fused into the tree kernel
+    dist_local / rank_combine  the two halves of dist (no communication)
     shard(n_global, world, rank) -> (offset, count) canonical shard
 """
 from __future__ import annotations
@@ -68,6 +70,12 @@ def _load():
         for f in ("nrmf_dist_d", "nrmf_dist_s"):
             getattr(L, f).argtypes = [i64, i64, i64, vp, vp, vp, sz, vp, vp]
             getattr(L, f).restype = i32
+        for f in ("nrmf_dist_local_d", "nrmf_dist_local_s"):
+            getattr(L, f).argtypes = [i64, i32, i32, i64, i64, vp, vp, i32, vp, sz, vp]
+            getattr(L, f).restype = i32
+        for f in ("nrmf_rank_combine_d", "nrmf_rank_combine_s"):
+            getattr(L, f).argtypes = [i64, i32, vp, vp, i32, vp]
+            getattr(L, f).restype = i32
         L.nrmf_dist_shard.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.nrmf_dist_shard.restype = i32
         L.nrmf_p2p_buffer_bytes.argtypes = []; L.nrmf_p2p_buffer_bytes.restype = sz
@@ -121,11 +129,29 @@ def tree_params(dtype) -> tuple[int, int, int]:
 
 # --------------------------------------------------------------- workspaces
 # Cached per (device, stream, kind).  The library clears the arrival counters
-# it uses on every call, so the initial contents do not matter.
+# it uses on every call, so the initial contents do not matter.  While
+# capture() records a graph, calls draw from that capture's own arena instead:
+# the graph keeps its workspaces alive (g._nrmf_ws) and shares them with no
+# other graph or direct call.
 _ws_cache: dict = {}
+_arena = threading.local()
 
 
 def _workspace(nbytes: int, device: torch.device, stream: torch.cuda.Stream, kind: str) -> torch.Tensor:
+    arena = getattr(_arena, "tensors", None)
+    if arena is not None:
+        # the n-th workspace of this kind requested by the captured call (the
+        # warm-up runs and the captured run make the same requests in order)
+        i = _arena.counts.get((device.index, kind), 0)
+        _arena.counts[(device.index, kind)] = i + 1
+        key = (device.index, kind, i)
+        t = arena.get(key)
+        if t is None or t.numel() < nbytes:
+            if torch.cuda.is_current_stream_capturing():
+                raise RuntimeError("nrmf.capture: the captured call requested a workspace its warm-up did not")
+            t = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+            arena[key] = t
+        return t
     key = (device.index, stream.cuda_stream, kind)
     t = _ws_cache.get(key)
     if t is None or t.numel() < nbytes:
@@ -135,6 +161,7 @@ def _workspace(nbytes: int, device: torch.device, stream: torch.cuda.Stream, kin
 
 
 def clear_workspaces():
+    """Drop the cached workspaces of direct calls (captured graphs own theirs)."""
     _ws_cache.clear()
 
 
@@ -277,6 +304,9 @@ class Comm:
         if self.handle:
             _load().nrmf_nccl_comm_destroy(self.handle)
             self.handle = None
+        for k, v in list(_comms.items()):
+            if v is self:
+                del _comms[k]
 
 
 _comms: dict = {}
@@ -285,7 +315,7 @@ _comms: dict = {}
 def comm_for(group=None) -> Comm:
     key = (id(group), torch.cuda.current_device())
     c = _comms.get(key)
-    if c is None:
+    if c is None or not c.handle:
         c = Comm(group)
         _comms[key] = c
     return c
@@ -317,6 +347,50 @@ def dist(x_local: torch.Tensor, n_global: int, group=None, comm: Comm | None = N
     return out
 
 
+def dist_local(x_local: torch.Tensor, n_global: int, world: int, rank: int, out: torch.Tensor | None = None,
+               top: str = "v1") -> torch.Tensor:
+    """The value of `rank`'s aligned subtree of the n_global-element tree
+    (x_local = its canonical shard, see shard()): the local half of dist(),
+    nrmf_dist_local_[ds].  No communication."""
+    if not x_local.is_cuda or not x_local.is_contiguous():
+        raise ValueError("nrmf.dist_local: contiguous CUDA tensor expected")
+    esz, c = _elem(x_local.dtype)
+    fl = _flags(top)
+    off, cnt = shard(n_global, world, rank)
+    if x_local.numel() != cnt:
+        raise ValueError(f"nrmf.dist_local: rank {rank} expects {cnt} elements, got {x_local.numel()}")
+    L = _load()
+    dev = x_local.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream(dev)
+        if out is None:
+            out = torch.empty((), dtype=x_local.dtype, device=dev)
+        ws = _workspace(L.nrmf_dist_workspace_bytes(n_global, world, esz), dev, s, "dist")
+        f = L.nrmf_dist_local_d if c == "d" else L.nrmf_dist_local_s
+        _check(f(n_global, world, rank, off, cnt, x_local.data_ptr() if cnt else None, out.data_ptr(), fl,
+                 ws.data_ptr(), ws.numel(), s.cuda_stream), "nrmf.dist_local")
+    return out
+
+
+def rank_combine(values: torch.Tensor, n_global: int, world: int, out: torch.Tensor | None = None,
+                 top: str = "v1") -> torch.Tensor:
+    """The rank tree over the ranks' dist_local values (a CUDA vector in rank
+    order, at least min(world, P2) entries): nrmf_rank_combine_[ds]."""
+    if not values.is_cuda or not values.is_contiguous():
+        raise ValueError("nrmf.rank_combine: contiguous CUDA tensor expected")
+    esz, c = _elem(values.dtype)
+    fl = _flags(top)
+    L = _load()
+    dev = values.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream(dev)
+        if out is None:
+            out = torch.empty((), dtype=values.dtype, device=dev)
+        f = L.nrmf_rank_combine_d if c == "d" else L.nrmf_rank_combine_s
+        _check(f(n_global, world, values.data_ptr(), out.data_ptr(), fl, s.cuda_stream), "nrmf.rank_combine")
+    return out
+
+
 class P2PGroup:
     """Peer-memory rank exchange for dist_p2p: allocates this rank's
     exchange buffer, all-gathers the CUDA IPC handles through the
@@ -342,17 +416,28 @@ class P2PGroup:
         dist.all_gather_object(handles, bytes(h.raw), group=group)
         self._opened = []
         ptrs = []
+        failed = None
         for r in range(self.world):
             if r == self.rank:
                 ptrs.append(buf.value)
                 continue
             p = ctypes.c_void_p()
-            _check(L.nrmf_p2p_open(ctypes.c_char_p(handles[r]), ctypes.byref(p)), "nrmf_p2p_open")
+            st = L.nrmf_p2p_open(ctypes.c_char_p(handles[r]), ctypes.byref(p))
+            if st != NRMF_OK:
+                failed = f"rank {self.rank} cannot map rank {r}'s buffer: {L.nrmf_status_str(st).decode()}"
+                break
             self._opened.append(p)
             ptrs.append(p.value)
+        # every rank learns whether every rank mapped every peer (this is also
+        # the barrier: every buffer is mapped before the first exchange)
+        status = [None] * self.world
+        dist.all_gather_object(status, failed, group=group)
+        bad = [m for m in status if m]
+        if bad:
+            self.close()
+            raise RuntimeError("nrmf.P2PGroup: " + "; ".join(bad))
         self.peers = torch.tensor(ptrs, dtype=torch.int64, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
-        dist.barrier(group=group)   # every buffer is mapped before the first exchange
 
     def close(self):
         L = _load()
@@ -448,18 +533,29 @@ def capture(fn, warmup: int = 1) -> "torch.cuda.CUDAGraph":
     graph; ``g.replay()`` then re-runs its launches -- counter memset, tree
     kernel, and for ``dist`` the NCCL allgather and the rank-tree kernel --
     with one launch.  The call is first run ``warmup`` times on
-    the capture stream, so its workspace exists before capture and the replay
-    reuses it; do not run other nrmf calls on that stream while the graph is
-    live.  Replays give the same bits as direct calls (tested)."""
+    the capture stream with workspaces from an arena of its own, which the
+    capture reuses and the returned graph keeps alive (``g._nrmf_ws``): no
+    other graph or direct call shares them, and clear_workspaces() does not
+    free them.  Replays give the same bits as direct calls (tested); replays
+    of one graph must not overlap each other."""
     cs = torch.cuda.Stream()
     cs.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(cs):
-        for _ in range(max(1, warmup)):
+    arena: dict = {}
+    prev = getattr(_arena, "tensors", None), getattr(_arena, "counts", None)
+    try:
+        _arena.tensors = arena
+        with torch.cuda.stream(cs):
+            for _ in range(max(1, warmup)):
+                _arena.counts = {}
+                fn()
+        torch.cuda.current_stream().wait_stream(cs)
+        g = torch.cuda.CUDAGraph()
+        _arena.counts = {}
+        with torch.cuda.graph(g, stream=cs):
             fn()
-    torch.cuda.current_stream().wait_stream(cs)
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=cs):
-        fn()
+    finally:
+        _arena.tensors, _arena.counts = prev
+    g._nrmf_ws = list(arena.values())
     return g
 
 

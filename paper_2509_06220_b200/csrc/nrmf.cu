@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -22,6 +23,7 @@
 #include "../../include/nrmf.h"
 #include "nrmf_device.cuh"
 #include "nrmf_internal.h"
+#include "nrmf_p2p.cuh"
 
 namespace nrmf {
 
@@ -93,7 +95,31 @@ struct TreeJob {
   int64_t nin[kMaxSteps];      // real (non-padding) inputs of step k (nin[0] = warp groups)
   int64_t val_off[kMaxSteps];  // vals offset of the inputs of step k
   int64_t cnt_off[kMaxSteps];  // cnt offset of the counters of step k
+  // rank exchange fused into the root's writer (nrmf_dist_p2p_[ds]): null = none
+  char* const* peers;  // device array of the ranks' exchange buffers (nrmf_p2p.cuh)
+  unsigned* p_err;     // nullable: set to 1 if a rank's value did not arrive in time
+  int p_world, p_rank, p_nr;
 };
+
+// The warp that evaluates the tree's root writes it.  With a fused rank
+// exchange (job.peers) the root is this rank's subtree value: the same warp
+// publishes it to every peer, waits for theirs and evaluates the rank tree
+// (rank_exchange, nrmf_p2p.cuh) before writing *out -- the distributed step
+// needs no launch after the tree kernel.  Warp-collective.
+// (Out of line, with scalar arguments: a reference to the kernel parameter
+// would make ptxas copy the whole TreeJob to the stack.)
+template <typename F>
+__device__ __noinline__ F exchange_root(char* const* peers, unsigned* err, int world, int rank, int nr, int cr,
+                                        F v) {
+  PeerArgs a{peers, world, rank, err};
+  return rank_exchange<F>(v, a, nr, cr);
+}
+template <typename F>
+__device__ __forceinline__ void write_root(const TreeJob<F>& job, F v) {
+  if (job.peers != nullptr)
+    v = exchange_root<F>(job.peers, job.p_err, job.p_world, job.p_rank, job.p_nr, job.top_cr, v);
+  if ((threadIdx.x & 31) == 0) *job.out = v;
+}
 
 // One warp evaluates the balanced tree over 2^f (f <= kMaxFanLg) consecutive
 // values vals[base ..] (entries >= nvals are +0).  All lanes return the value.
@@ -212,12 +238,17 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != expect - 1) return;
     NRMF_TRACE(2, k, 0);
-    fence_acq_rel_gpu();  // acquire: the other arrivals' values (released by their atomics) are visible
-    if (lane == 0) job.cnt[job.cnt_off[k] + g] = 0u;  // ready for the next call
+    if (lane == 0) {
+      // acquire by the lane that read the counter: the other arrivals' values
+      // (released by their atomics) are visible to it ...
+      fence_acq_rel_gpu();
+      job.cnt[job.cnt_off[k] + g] = 0u;  // ready for the next call
+    }
+    __syncwarp();  // ... and to every lane of the warp (bar.warp.sync orders memory)
     const F v = warp_group_bal<F, WIDE>(job.vals + job.val_off[k], job.nin[k], g * fan, f, job.top_cr);
     NRMF_TRACE(3, k, 0);
     if (k + 1 == job.nsteps) {
-      if (lane == 0) *job.out = v;
+      write_root(job, v);
       return;
     }
     if (lane == 0) {
@@ -526,7 +557,11 @@ __device__ void cta_try(const TreeJob<F>& job, uint32_t cta_s, int rr, int b, in
   if (lane == 0 && ld_volatile_shared_u32(ts) == (unsigned)rr && ld_volatile_shared_u32(cs) == (unsigned)expect)
     got = cas_acq_rel_cta_shared(ts, (unsigned)rr, (unsigned)rr | kClaimed) == (unsigned)rr;
   if (!__shfl_sync(0xffffffffu, got, 0)) return;
-  fence_acq_rel_cta();  // every arrival's value is visible to every lane
+  // lane 0 read the complete count (written by the arrivals' release adds):
+  // its fence makes every arrival's value visible to it, and __syncwarp
+  // extends that ordering to the warp's other lanes
+  if (lane == 0) fence_acq_rel_cta();
+  __syncwarp();
   NRMF_TRACE(2, 15, 0);
   F v = F(0);
   if (lane < expect) ld_shared(vs + lane * (uint32_t)sizeof(F), v);
@@ -547,7 +582,7 @@ __device__ void cta_try(const TreeJob<F>& job, uint32_t cta_s, int rr, int b, in
   }
   NRMF_TRACE(3, 15, 0);
   if (job.nsteps == 1) {
-    if (lane == 0) *job.out = v;
+    write_root(job, v);
     return;
   }
   unsigned old1 = 0;
@@ -777,7 +812,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     continue;
 #endif
     if (job.nsteps == 0) {  // the warp group is the whole tree
-      if (lane == 0) *job.out = gv[0];
+      write_root(job, gv[0]);
       continue;
     }
     if (kStream && job.cta_step0) {
@@ -873,7 +908,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   NRMF_TRACE(1, 0, 0);
   if (!job.combine) return;
   if (job.nsteps == 0) {
-    if (lane == 0) *job.out = gv;
+    write_root(job, gv);
     return;
   }
   unsigned old = 0;
@@ -964,6 +999,7 @@ static int device_sms() {
 
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+constexpr uintptr_t kWsAlign = 16;  // nrmf.h: workspaces are 16-byte aligned
 
 // Plan of the combine over p2 tiles of which n_items are real: g0 levels
 // inside each warp group, then steps of 6 levels (fan-in 64); first_fan = 4:
@@ -1040,6 +1076,9 @@ static TreeJob<F> make_job(const F* x, int64_t n_items, int64_t tpc, int64_t ld,
   job.g0 = pl.g0;
   job.cta_minor = 0;
   job.cta_step0 = 0;
+  job.peers = nullptr;
+  job.p_err = nullptr;
+  job.p_world = job.p_rank = job.p_nr = 0;
   job.nsteps = pl.nsteps;
   for (int k = 0; k < kMaxSteps; ++k) {
     job.lg_fan[k] = pl.lg_fan[k];
@@ -1048,6 +1087,16 @@ static TreeJob<F> make_job(const F* x, int64_t n_items, int64_t tpc, int64_t ld,
     job.cnt_off[k] = pl.cnt_off[k];
   }
   return job;
+}
+
+template <typename F>
+static void set_exchange(TreeJob<F>& job, const RankExchange* rx) {
+  if (rx == nullptr) return;
+  job.peers = rx->peers;
+  job.p_err = rx->err;
+  job.p_world = rx->world;
+  job.p_rank = rx->rank;
+  job.p_nr = rx->nr;
 }
 
 #ifndef NRMF_NT
@@ -1063,23 +1112,31 @@ static size_t kernel_smem() {
   return (size_t)kWarps * kStages * kBatchBytes + (size_t)kWarps * kStages * 8;
 }
 
+// Function attributes (the dynamic shared memory opt-in) belong to a device's
+// context: they are set, and the occupancy cached, once per device.
+constexpr int kMaxDevices = 64;
 template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false>
 static int blocks_per_sm() {
-  static int cached = 0;
-  if (cached == 0) {
-    const size_t sm = kernel_smem<F, TMA, STREAM>();
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM, GAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sm);
-    int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM, GAP>, kThreads,
-                                                      sm) !=
-            cudaSuccess ||
-        b < 1)
-      b = 1;
-    cached = b;
-  }
-  return cached;
+  static std::atomic<int> cached[kMaxDevices];
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return 1;
+  int b = cached[dev].load(std::memory_order_acquire);
+  if (b != 0) return b;
+  std::lock_guard<std::mutex> lock(mu);
+  b = cached[dev].load(std::memory_order_relaxed);
+  if (b != 0) return b;
+  const size_t sm = kernel_smem<F, TMA, STREAM>();
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM, GAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM, GAP>, kThreads, sm) !=
+          cudaSuccess ||
+      b < 1)
+    b = 1;
+  cached[dev].store(b, std::memory_order_release);
+  return b;
 }
 
 static int g_grid_override = 0;  // test hook: force a grid size (0 = automatic)
@@ -1091,7 +1148,7 @@ static int g_gap_stream = 1;     // test hook: gapped column blocks on the strea
 template <typename F>
 static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int64_t len, int64_t p2,
                        F* tile_out, F* out, int combine, void* ws, size_t ws_bytes, bool vec,
-                       cudaStream_t s, int top_cr) {
+                       cudaStream_t s, int top_cr, const RankExchange* rx = nullptr) {
   if (n_items == 0) return NRMF_OK;
   if (n_items >= (int64_t(1) << 31) - 64) return NRMF_EINVAL;  // kernels index tiles/groups in 32 bits (n < 2^43)
   // contiguous tiles (a vector, or whole columns of T-multiple length stored
@@ -1123,6 +1180,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
       if (combine && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
         return NRMF_ECUDA;
       TreeJob<F> job = make_job(x, n_items, tpc, ld, len, tile_out, out, combine, top_cr, ws, cnt_bytes, pl);
+      set_exchange(job, rx);
       if (vec) nrmf_split_kernel<F, kVec><<<(unsigned)n_groups, kSplitWarps * 32, 0, s>>>(job);
       else nrmf_split_kernel<F, kScalar><<<(unsigned)n_groups, kSplitWarps * 32, 0, s>>>(job);
       return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
@@ -1180,6 +1238,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   if (combine && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
     return NRMF_ECUDA;
   TreeJob<F> job = make_job(x, n_items, tpc, ld, len, tile_out, out, combine, top_cr, ws, cnt_bytes, pl);
+  set_exchange(job, rx);
   const int64_t n_groups = (n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0;
   job.cta_minor = n_groups < grid * kWarps;
   job.cta_step0 = cta_step0 ? 1 : 0;
@@ -1202,7 +1261,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
 
 template <typename F>
 int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes, cudaStream_t s,
-              int top_cr) {
+              int top_cr, const RankExchange* rx) {
   // Evaluate the balanced tree over p2 tiles (p2 >= ceil(n/T), power of two)
   // of x[0..n) padded with +0; *out = root.  Caller validated arguments.
   const int64_t nt = (n + kTile - 1) / kTile;
@@ -1211,11 +1270,13 @@ int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_byt
     return NRMF_OK;
   }
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
-  return launch_tree<F>(x, nt, nt, 0, n, p2, nullptr, out, 1, ws, ws_bytes, vec, s, top_cr);
+  return launch_tree<F>(x, nt, nt, 0, n, p2, nullptr, out, 1, ws, ws_bytes, vec, s, top_cr, rx);
 }
 
-template int tree_eval<double>(int64_t, const double*, int64_t, double*, void*, size_t, cudaStream_t, int);
-template int tree_eval<float>(int64_t, const float*, int64_t, float*, void*, size_t, cudaStream_t, int);
+template int tree_eval<double>(int64_t, const double*, int64_t, double*, void*, size_t, cudaStream_t, int,
+                               const RankExchange*);
+template int tree_eval<float>(int64_t, const float*, int64_t, float*, void*, size_t, cudaStream_t, int,
+                              const RankExchange*);
 
 template <typename F>
 int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s, int top_cr) {
@@ -1232,7 +1293,7 @@ template <typename F>
 static int nrmf_vec(int64_t n, const F* x, F* out, int flags, void* ws, size_t ws_bytes, void* stream) {
   if (n < 0 || out == nullptr || (n > 0 && (x == nullptr || ws == nullptr))) return NRMF_EINVAL;
   if ((reinterpret_cast<uintptr_t>(x) % sizeof(F)) != 0 ||
-      (reinterpret_cast<uintptr_t>(out) % sizeof(F)) != 0)
+      (reinterpret_cast<uintptr_t>(out) % sizeof(F)) != 0 || (reinterpret_cast<uintptr_t>(ws) % kWsAlign) != 0)
     return NRMF_EALIGN;
   const int64_t nt = (n + kTile - 1) / kTile;
   return tree_eval<F>(n, x, pow2_ceil(std::max<int64_t>(nt, 1)), out, ws, ws_bytes,
@@ -1264,7 +1325,7 @@ static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F*
   if (cols > 0 && col_norms == nullptr) return NRMF_EINVAL;
   if (rows > 0 && cols > 0 && (A == nullptr || ws == nullptr)) return NRMF_EINVAL;
   if (reinterpret_cast<uintptr_t>(A) % sizeof(F) || reinterpret_cast<uintptr_t>(col_norms) % sizeof(F) ||
-      reinterpret_cast<uintptr_t>(frob) % sizeof(F))
+      reinterpret_cast<uintptr_t>(frob) % sizeof(F) || reinterpret_cast<uintptr_t>(ws) % kWsAlign)
     return NRMF_EALIGN;
   if (cols == 0) {
     if (frob && cudaMemsetAsync(frob, 0, sizeof(F), s) != cudaSuccess) return NRMF_ECUDA;
@@ -1357,7 +1418,8 @@ static int nrmf_host_impl(int64_t n, const F* host_x, F* host_out, int flags, vo
   const int cr = flags & NRMF_TOP_CR;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n < 0 || host_out == nullptr || ws == nullptr || (n > 0 && host_x == nullptr)) return NRMF_EINVAL;
-  if (reinterpret_cast<uintptr_t>(host_x) % sizeof(F)) return NRMF_EALIGN;
+  if (reinterpret_cast<uintptr_t>(host_x) % sizeof(F) || reinterpret_cast<uintptr_t>(ws) % kWsAlign)
+    return NRMF_EALIGN;
   if (ws_bytes < host_ws_bytes(n, sizeof(F))) return NRMF_EWORKSPACE;
   const int64_t nt = std::max<int64_t>((n + kTile - 1) / kTile, 1);
   const int64_t p2 = pow2_ceil(nt);

@@ -29,6 +29,7 @@ namespace nrmf {
 namespace {
 
 constexpr int64_t kTileE = 4096;
+constexpr uintptr_t kWsAlign = 16;  // nrmf.h: workspaces are 16-byte aligned
 
 struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
@@ -121,53 +122,91 @@ size_t dist_ws(int64_t n, int world, size_t esz) {
   return tree_workspace(p2l, esz) + 256 + align_up((size_t)world * esz, 256);
 }
 
+// The rank's step of the distributed tree (shared by nrmf_dist_local_[ds],
+// nrmf_dist_[ds] and nrmf_dist_p2p_[ds], so all of them run the same kernels):
+// validate the canonical shard, then reduce the rank's aligned subtree of the
+// global tile tree (size p2l, +0 padded) into *local -- the same tree kernel
+// as nrmf_[ds].  A rank that owns an all-padding subtree or none contributes +0.
+// rx (nullable): the peer exchange fused into the tree kernel's root writer;
+// *local then receives the rank tree's root (the global norm).
 template <typename F>
-int dist_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, void* ws,
-              size_t ws_bytes, void* comm_v, void* stream, int flags) {
+__global__ void __launch_bounds__(32) p2p_exchange_kernel(const F* local, PeerArgs a, int nr, int cr, F* out);
+
+template <typename F>
+int local_step(int64_t n, int world, int rank, int64_t offset, int64_t count, const F* x, F* local, int flags,
+               void* ws, size_t ws_bytes, cudaStream_t s, const RankExchange* rx) {
   if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
   const int cr = flags & NRMF_TOP_CR;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const NcclApi* api = nccl();
-  if (api == nullptr) return NRMF_ENCCL;
-  if (comm_v == nullptr || out == nullptr || ws == nullptr || n < 0) return NRMF_EINVAL;
+  if (local == nullptr || ws == nullptr || n < 0 || world < 1 || rank < 0 || rank >= world) return NRMF_EINVAL;
   if (count > 0 && x == nullptr) return NRMF_EINVAL;
-  if (reinterpret_cast<uintptr_t>(x) % sizeof(F) || reinterpret_cast<uintptr_t>(out) % sizeof(F))
+  if (reinterpret_cast<uintptr_t>(x) % sizeof(F) || reinterpret_cast<uintptr_t>(local) % sizeof(F))
     return NRMF_EALIGN;
-  ncclComm_t comm = static_cast<ncclComm_t>(comm_v);
-  int world = 0, rank = 0;
-  if (api->CommCount(comm, &world) != ncclSuccess || api->CommUserRank(comm, &rank) != ncclSuccess)
-    return NRMF_ENCCL;
+  if (reinterpret_cast<uintptr_t>(ws) % kWsAlign) return NRMF_EALIGN;
   if (!is_pow2(world)) return NRMF_ESHARD;
   int64_t off = 0, cnt = 0;
   const int64_t p2l = shard(n, world, rank, &off, &cnt);
   if (off != offset || cnt != count) return NRMF_ESHARD;
   if (ws_bytes < dist_ws(n, world, sizeof(F))) return NRMF_EWORKSPACE;
-
   const int64_t nt = (n + kTileE - 1) / kTileE;
   const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
   const int64_t p2ws = world <= P2 ? P2 / world : 1;
-  char* p = static_cast<char*>(ws);
   const size_t tws = tree_workspace(p2ws, sizeof(F));
-  void* tree_ws = p;
+  if (p2l > 0 && cnt > 0) return tree_eval<F>(cnt, x, p2l, local, ws, tws, s, cr, rx);
+  // no data here: the subtree value is +0
+  F* zero = reinterpret_cast<F*>(static_cast<char*>(ws) + tws);
+  if (cudaMemsetAsync(rx ? zero : local, 0, sizeof(F), s) != cudaSuccess) return NRMF_ECUDA;
+  if (rx == nullptr) return NRMF_OK;
+  PeerArgs a{rx->peers, rx->world, rx->rank, rx->err};
+  p2p_exchange_kernel<F><<<1, 32, 0, s>>>(zero, a, rx->nr, cr, local);
+  return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
+}
+
+// The rank tree: the balanced tree over the values of the min(world, P2)
+// ranks that own part of the tile tree, in rank order (e:hr; a FIXED order,
+// P:1077-1084).
+template <typename F>
+int rank_combine(int64_t n, int world, const F* values, F* out, int flags, cudaStream_t s) {
+  if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
+  if (values == nullptr || out == nullptr || n < 0 || world < 1) return NRMF_EINVAL;
+  if (reinterpret_cast<uintptr_t>(values) % sizeof(F) || reinterpret_cast<uintptr_t>(out) % sizeof(F))
+    return NRMF_EALIGN;
+  if (!is_pow2(world)) return NRMF_ESHARD;
+  const int64_t nt = (n + kTileE - 1) / kTileE;
+  const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
+  const int64_t nr = std::min<int64_t>(world, P2);
+  return bal_eval<F>(values, nr, nr, out, s, flags & NRMF_TOP_CR);
+}
+
+template <typename F>
+int dist_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, void* ws,
+              size_t ws_bytes, void* comm_v, void* stream, int flags) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const NcclApi* api = nccl();
+  if (api == nullptr) return NRMF_ENCCL;
+  if (comm_v == nullptr || out == nullptr || ws == nullptr || n < 0) return NRMF_EINVAL;
+  ncclComm_t comm = static_cast<ncclComm_t>(comm_v);
+  int world = 0, rank = 0;
+  if (api->CommCount(comm, &world) != ncclSuccess || api->CommUserRank(comm, &rank) != ncclSuccess)
+    return NRMF_ENCCL;
+  if (reinterpret_cast<uintptr_t>(out) % sizeof(F)) return NRMF_EALIGN;
+  if (!is_pow2(world)) return NRMF_ESHARD;
+  const int64_t nt = (n + kTileE - 1) / kTileE;
+  const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
+  const size_t tws = tree_workspace(world <= P2 ? P2 / world : 1, sizeof(F));
+  char* p = static_cast<char*>(ws);
   F* local = reinterpret_cast<F*>(p + tws);
   F* gathered = reinterpret_cast<F*>(p + tws + 256);
-
-  int st = NRMF_OK;
-  if (p2l > 0 && cnt > 0) {
-    st = tree_eval<F>(cnt, x, p2l, local, tree_ws, tws, s, cr);
-  } else if (cudaMemsetAsync(local, 0, sizeof(F), s) != cudaSuccess) {
-    st = NRMF_ECUDA;  // rank owns an all-padding subtree (value +0) or none
-  }
+  int st = local_step<F>(n, world, rank, offset, count, x, local, flags, ws, ws_bytes, s, nullptr);
   if (st != NRMF_OK) return st;
   const ncclDataType_t dt = sizeof(F) == 8 ? ncclFloat64 : ncclFloat32;
   if (api->AllGather(local, gathered, 1, dt, comm, s) != ncclSuccess) return NRMF_ENCCL;
-  // rank tree: the top levels over the ranks that own part of the tree
-  const int64_t nr = std::min<int64_t>(world, P2);
-  return bal_eval<F>(gathered, nr, nr, out, s, cr);
+  return rank_combine<F>(n, world, gathered, out, flags, s);
 }
 
 // ---------------------------------------------------------------- peer memory
-// The rank level through peer memory (nrmf_p2p.cuh): one warp per rank.
+// The rank level through peer memory (nrmf_p2p.cuh): one warp per rank.  Used
+// on its own only by a rank without data (and by the emulation test); with
+// data the exchange runs inside the tree kernel (write_root, nrmf.cu).
 template <typename F>
 __global__ void __launch_bounds__(32) p2p_exchange_kernel(const F* local, PeerArgs a, int nr, int cr, F* out) {
   const F v = rank_exchange<F>(*local, a, nr, cr);
@@ -188,36 +227,13 @@ __global__ void __launch_bounds__(32) p2p_emulate_kernel(const F* values, PeerAr
 template <typename F>
 int dist_p2p_impl(int64_t n, int64_t offset, int64_t count, const F* x, F* out, int flags, void* ws,
                   size_t ws_bytes, const void* peers, int world, int rank, unsigned* err, void* stream) {
-  if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
-  const int cr = flags & NRMF_TOP_CR;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (peers == nullptr || out == nullptr || ws == nullptr || n < 0) return NRMF_EINVAL;
   if (world < 1 || world > kP2PMaxRanks || rank < 0 || rank >= world) return NRMF_EINVAL;
-  if (!is_pow2(world)) return NRMF_ESHARD;
-  if (count > 0 && x == nullptr) return NRMF_EINVAL;
-  if (reinterpret_cast<uintptr_t>(x) % sizeof(F) || reinterpret_cast<uintptr_t>(out) % sizeof(F))
-    return NRMF_EALIGN;
-  int64_t off = 0, cnt = 0;
-  const int64_t p2l = shard(n, world, rank, &off, &cnt);
-  if (off != offset || cnt != count) return NRMF_ESHARD;
-  if (ws_bytes < dist_ws(n, world, sizeof(F))) return NRMF_EWORKSPACE;
   const int64_t nt = (n + kTileE - 1) / kTileE;
   const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
-  const int64_t p2ws = world <= P2 ? P2 / world : 1;
-  char* p = static_cast<char*>(ws);
-  const size_t tws = tree_workspace(p2ws, sizeof(F));
-  F* local = reinterpret_cast<F*>(p + tws);
-  int st = NRMF_OK;
-  if (p2l > 0 && cnt > 0) {
-    st = tree_eval<F>(cnt, x, p2l, local, p, tws, s, cr);
-  } else if (cudaMemsetAsync(local, 0, sizeof(F), s) != cudaSuccess) {
-    st = NRMF_ECUDA;
-  }
-  if (st != NRMF_OK) return st;
-  PeerArgs a{static_cast<char* const*>(peers), world, rank, err};
-  const int nr = (int)std::min<int64_t>(world, P2);
-  p2p_exchange_kernel<F><<<1, 32, 0, s>>>(local, a, nr, cr, out);
-  return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
+  RankExchange rx{static_cast<char* const*>(peers), err, world, rank, (int)std::min<int64_t>(world, P2)};
+  return local_step<F>(n, world, rank, offset, count, x, out, flags, ws, ws_bytes, s, &rx);
 }
 
 template <typename F>
@@ -321,6 +337,23 @@ int nrmf_dist_ex_d(int64_t n_global, int64_t offset, int64_t count, const double
 int nrmf_dist_ex_s(int64_t n_global, int64_t offset, int64_t count, const float* x_local, float* out,
                    int flags, void* ws, size_t ws_bytes, void* nccl_comm, void* stream) {
   return dist_impl<float>(n_global, offset, count, x_local, out, ws, ws_bytes, nccl_comm, stream, flags);
+}
+
+int nrmf_dist_local_d(int64_t n_global, int world, int rank, int64_t offset, int64_t count, const double* x_local,
+                      double* local_out, int flags, void* ws, size_t ws_bytes, void* stream) {
+  return local_step<double>(n_global, world, rank, offset, count, x_local, local_out, flags, ws, ws_bytes,
+                            static_cast<cudaStream_t>(stream), nullptr);
+}
+int nrmf_dist_local_s(int64_t n_global, int world, int rank, int64_t offset, int64_t count, const float* x_local,
+                      float* local_out, int flags, void* ws, size_t ws_bytes, void* stream) {
+  return local_step<float>(n_global, world, rank, offset, count, x_local, local_out, flags, ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream), nullptr);
+}
+int nrmf_rank_combine_d(int64_t n_global, int world, const double* values, double* out, int flags, void* stream) {
+  return rank_combine<double>(n_global, world, values, out, flags, static_cast<cudaStream_t>(stream));
+}
+int nrmf_rank_combine_s(int64_t n_global, int world, const float* values, float* out, int flags, void* stream) {
+  return rank_combine<float>(n_global, world, values, out, flags, static_cast<cudaStream_t>(stream));
 }
 
 int nrmf_cols_dist_shard(int64_t cols_global, int world, int rank, int64_t* col_offset, int64_t* col_count) {

@@ -6,10 +6,18 @@
 #include <cstdint>
 
 namespace nrmf {
+// Rank exchange fused into the tree kernel (nrmf_p2p.cuh): the warp that
+// evaluates the local root publishes it to the peers, waits for theirs and
+// writes the rank tree's root instead.
+struct RankExchange {
+  char* const* peers;  // device array of world buffer pointers
+  unsigned* err;       // nullable
+  int world, rank, nr;
+};
 // Balanced tree over p2 tiles of x[0..n) (zero padded) -> *out (device).
 template <typename F>
 int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes, cudaStream_t s,
-              int top_cr);
+              int top_cr, const RankExchange* rx = nullptr);
 // Balanced tree over vals[0..P) (entries >= nvals are +0) -> *out, one CTA.
 template <typename F>
 int bal_eval(const F* vals, int64_t nvals, int64_t P, F* out, cudaStream_t s, int top_cr);

@@ -73,6 +73,22 @@ def test_argument_errors_without_gpu(L):
     assert L.nrmf_cols_d(10, 2, 5, 16, 16, None, 1024, 1 << 20, None) == 1   # ld < rows
 
 
+def test_workspace_alignment_is_checked_at_enqueue(L):
+    # a workspace not 16-byte aligned is NRMF_EALIGN (nrmf.h), not an
+    # asynchronous fault; checked before any device work
+    big = 1 << 20
+    assert L.nrmf_d(10, 16, 16, 1024 + 8, big, None) == 2
+    assert L.nrmf_s(10, 16, 16, 1024 + 4, big, None) == 2
+    assert L.nrmf_cols_d(10, 2, 10, 16, 16, None, 1024 + 8, big, None) == 2
+    assert L.nrmf_host_d(10, 16, 16, 1024 + 8, 1 << 30, None) == 2
+    assert L.nrmf_dist_local_d(10, 1, 0, 0, 10, 16, 16, 0, 1024 + 8, big, None) == 2
+    assert L.nrmf_dist_local_d(10, 2, 2, 0, 10, 16, 16, 0, 1024, big, None) == 1      # rank >= world
+    assert L.nrmf_dist_local_d(10, 2, 0, 0, 9, 16, 16, 0, 1024, big, None) == 4       # not the canonical shard
+    assert L.nrmf_dist_local_d(10, 3, 0, 0, 10, 16, 16, 0, 1024, big, None) == 4      # world not a power of two
+    assert L.nrmf_rank_combine_d(10, 2, 12, 16, 0, None) == 2                          # values misaligned
+    assert L.nrmf_rank_combine_d(10, 2, 16, 16, 2, None) == 1                          # unknown flag
+
+
 @pytest.mark.parametrize("n,G", [(1 << 30, 1), (1 << 30, 2), (1 << 30, 8), (5, 8), (4097, 4),
                                  (17 * 4096 - 3, 8), (0, 2)])
 def test_shard_partition_matches_oracle_reading(n, G):

@@ -39,6 +39,47 @@ def test_reference_arm_nonzero_rank_exits_quietly():
 
 
 
+def test_gpus_beyond_the_visible_devices_fail_fast():
+    """--gpus N without a torchrun environment re-execs under torch.distributed.run;
+    with fewer than N visible GPUs it exits non-zero at once (never silently
+    one GPU under an N-GPU label)."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode != 0
+    assert "needs 2 GPUs" in p.stderr
+    assert not [ln for ln in p.stdout.splitlines() if ln.strip().startswith("{")]
+
+
+def test_world_size_mismatch_is_an_error():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", CUDA_VISIBLE_DEVICES="")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode != 0 and "WORLD_SIZE=1" in p.stderr
+
+
+@pytest.mark.gpu
+def test_gpu_arm_reexec_under_torchrun():
+    """The re-exec branch: bench.py launches itself under
+    torch.distributed.run (forced with --launcher torchrun at --gpus 1 on this
+    one-GPU box); the line's n_gpus equals --gpus and its result is the N = 1
+    tree's bits (the oracle's value of the workload)."""
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--launcher", "torchrun",
+                        "--steps", "3", "--warmup", "3", "--no-extras", "--e2e-steps", "1"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["ranks_same_bits"] and d["same_bits_as_1gpu_tree"] is True
+    assert d["result_hex"] == _c3_oracle_hex() and len(d["per_rank_ms"]) == 1
+
+
 @pytest.mark.gpu
 def test_gpu_arm_prints_one_contract_line():
     """bench.py's own arm on the GPU (short run): one JSON line carrying the
@@ -92,7 +133,8 @@ def test_gpu_arm_distributed_step_on_one_rank(p2p):
     d = json.loads(lines[0])
     assert d["rank_exchange"] == ("p2p" if p2p == "1" else "nccl_allgather")
     assert d["graph"] and d["e2e"]["same_bits"] and d["allgather_8B_us"] > 0
-    assert d["result_hex"] == _c3_oracle_hex()
+    assert d["result_hex"] == _c3_oracle_hex() and d["same_bits_as_1gpu_tree"] is True
+    assert d["gpu_launches"] == d["steps"] * (1 if p2p == "1" else 2)
 
 
 _C3_HEX = []
@@ -100,12 +142,15 @@ _C3_HEX = []
 
 def _c3_oracle_hex():
     """The oracle's value of bench.py's C3 workload (n = 2^30 N(0,1), seed 1),
-    big-endian hex as bench.py prints it (computed once, ~15 s on one core)."""
+    big-endian hex as bench.py prints it (computed once, ~15 s on one core);
+    it must equal the golden file bench.py reads (tools/make_golden_bench.py)."""
     if not _C3_HEX:
         import numpy as np
 
+        import golden_values
         import nrmf_inputs as gen
         import oracle
         x = gen.normal(1, 1 << 30, 0, dtype=np.float64)
         _C3_HEX.append(np.asarray(oracle.nrmf(x), dtype=np.float64).tobytes()[::-1].hex())
+        assert golden_values.hex_of("c3") == _C3_HEX[0]
     return _C3_HEX[0]

@@ -94,3 +94,27 @@ def test_dist_graph_replay_world1(nrmf):
         nrmf._comms.clear()
         if created:
             td.destroy_process_group()
+
+
+def test_graphs_own_their_workspaces(nrmf):
+    """each captured graph owns its workspace (g._nrmf_ws), so two
+    graphs never share arrival counters, a later capture that needs more space
+    cannot free an earlier graph's, and clear_workspaces() leaves them alive."""
+    xs = [gen.normal(11 + i, n, dtype=np.float64) for i, n in enumerate((300 * T + 11, 3000 * T + 5))]
+    xd = [torch.from_numpy(x).cuda() for x in xs]
+    outs = [torch.empty((), dtype=torch.float64, device="cuda") for _ in xs]
+    gs = [nrmf.capture(lambda x=x, o=o: nrmf.norm(x, out=o)) for x, o in zip(xd, outs)]
+    ptrs = [{t.data_ptr() for t in g._nrmf_ws} for g in gs]
+    assert ptrs[0] and ptrs[1] and not (ptrs[0] & ptrs[1])
+    nrmf.clear_workspaces()
+    torch.cuda.empty_cache()
+    junk = torch.full((1 << 26,), 0xAB, dtype=torch.uint8, device="cuda")  # reuse freed blocks, if any
+    side = torch.cuda.Stream()
+    for _ in range(3):
+        gs[0].replay()
+        with torch.cuda.stream(side):
+            gs[1].replay()                   # concurrently on another stream
+        torch.cuda.synchronize()
+        for o, x in zip(outs, xs):
+            assert bits(o.cpu().numpy(), np.float64) == bits(oracle.nrmf(x), np.float64)
+    del junk

@@ -6,8 +6,8 @@ protocol -- P2P value stores, release flags, parity halves per epoch, the rank
 tree -- is run with `world` ranks emulated as the CTAs of ONE cooperative
 launch, each rank with its own buffer; every rank's result must equal the
 oracle's rank tree bit for bit, over several epochs without resetting the
-buffers.  The full dist_p2p call (tree kernel + exchange kernel, IPC setup) is
-run on a 1-rank group against the oracle."""
+buffers.  The full dist_p2p call (the tree kernel with the exchange at its
+root, IPC setup) is run on a 1-rank group against the oracle."""
 import os
 
 import numpy as np
@@ -62,9 +62,15 @@ def test_exchange_protocol_emulated_ranks(nrmf, dt, world, top):
             nrmf.lib().nrmf_p2p_free(p)
 
 
-def test_dist_p2p_world1(nrmf):
-    """dist_p2p on a 1-rank group (IPC handle, peer array, exchange kernel with
-    the rank's own buffer) equals nrmf_d / nrmf_s and the oracle, over calls."""
+@pytest.mark.parametrize("grid", [0, 1, 2, 5])
+def test_dist_p2p_world1(nrmf, grid):
+    """dist_p2p on a 1-rank group (IPC handle, peer array, the exchange fused
+    into the tree kernel's root writer with the rank's own buffer) equals the
+    oracle, over calls.  Every place the root can be written: the split
+    kernel's climb (grid 0, small n) and its single group (n <= T), the
+    persistent kernel's single group (forced grid 1, n = 8T), its climbs and
+    CTA combine step (forced grids 1/2/5, and grid 0 at 2^26 + 5), and a rank
+    without data (n = 0: +0 through the separate exchange kernel)."""
     import torch.distributed as td
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29547")
@@ -73,15 +79,22 @@ def test_dist_p2p_world1(nrmf):
         td.init_process_group("gloo", rank=0, world_size=1)
         created = True
     pg = None
+    nrmf._debug_set_grid(grid)
     try:
         pg = nrmf.P2PGroup()
+        sizes = [0, 1, 4097, 8 * T, 300 * T + 5, (1 << 22) + 3] + ([(1 << 26) + 5] if grid == 0 else [])
         for dt in (np.float64, np.float32):
-            for n in (1, 4097, 300 * T + 5):
-                x = gen.normal(n, n, dtype=dt)
-                r = nrmf.dist_p2p(torch.from_numpy(x).cuda(), n, pg).cpu().numpy()
-                assert np.asarray(r, dtype=dt).tobytes() == np.asarray(oracle.nrmf(x), dtype=dt).tobytes()
+            for n in sizes:
+                x = gen.normal(n + 1, n, dtype=dt)
+                for _ in range(2):
+                    r = nrmf.dist_p2p(torch.from_numpy(x).cuda(), n, pg).cpu().numpy()
+                    assert np.asarray(r, dtype=dt).tobytes() == np.asarray(oracle.nrmf(x), dtype=dt).tobytes(), n
+                rc = nrmf.dist_p2p(torch.from_numpy(x).cuda(), n, pg, top="cr").cpu().numpy()
+                assert np.asarray(rc, dtype=dt).tobytes() == np.asarray(oracle.nrmf(x, top="cr"),
+                                                                         dtype=dt).tobytes(), n
         assert int(pg.err.item()) == 0
     finally:
+        nrmf._debug_set_grid(0)
         if pg is not None:
             pg.close()
         if created:

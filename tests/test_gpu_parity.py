@@ -299,7 +299,9 @@ def test_hypot_many_pairs_via_columns(nrmf, dt):
     a = np.ldexp(rng.uniform(1, 2, m), rng.integers(emin, emax, m)).astype(dt)
     b = np.ldexp(rng.uniform(1, 2, m), rng.integers(emin, emax, m)).astype(dt)
     k = m // 4
-    b[:k] = (a[:k] * np.ldexp(1.0, rng.integers(-3, 3, k))).astype(dt)   # q near 1
+    # q near 1 (rounding-sensitive S = fma(q,q,1)): |b| in [|a|/2, |a|), never
+    # beyond |a|, so nothing overflows near the top of the range
+    b[:k] = (a[:k].astype(np.float64) * rng.uniform(0.5, 1.0, k)).astype(dt)
     a[k:2 * k] = np.ldexp(rng.integers(0, 1 << 20, k), emin).astype(dt)   # subnormals
     A = np.empty(2 * m, dtype=dt)
     A[0::2], A[1::2] = a, b
