@@ -79,6 +79,16 @@ typedef enum {
  *   (+inf if either operand is infinite, else NaN if either is NaN). */
 #define NRMF_TOP_CR 1
 
+/* NRMF_WS_CLEAN: the caller guarantees that the workspace's arrival counters
+ *   are zero on entry: ws was zero-filled before its first call and has since
+ *   been used only by calls with identical arguments (e.g. the warm-up and the
+ *   replays of one captured CUDA graph), each completed before the next began.
+ *   Every completed call leaves its counters zero, so the guarantee carries
+ *   over; the call then skips its counter memset and is a single kernel (one
+ *   graph node).  Without it (the default) the contents of ws never matter.
+ *   Ignored by the host-input calls, which always clear their counters. */
+#define NRMF_WS_CLEAN 2
+
 /* Human-readable name of a status code (static string). */
 const char *nrmf_status_str(int status);
 
@@ -95,7 +105,8 @@ size_t nrmf_workspace_bytes(int64_t n, int elem_bytes);
 int nrmf_d(int64_t n, const double *x, double *out, void *ws, size_t ws_bytes, void *stream);
 int nrmf_s(int64_t n, const float *x, float *out, void *ws, size_t ws_bytes, void *stream);
 
-/* The same with flags (NRMF_TOP_CR or 0); flags 0 is bitwise nrmf_[ds]. */
+/* The same with flags (NRMF_TOP_CR | NRMF_WS_CLEAN or 0); flags 0 is bitwise
+ * nrmf_[ds] (NRMF_WS_CLEAN never changes a result, only the launches). */
 int nrmf_ex_d(int64_t n, const double *x, double *out, int flags, void *ws, size_t ws_bytes, void *stream);
 int nrmf_ex_s(int64_t n, const float *x, float *out, int flags, void *ws, size_t ws_bytes, void *stream);
 
@@ -198,7 +209,8 @@ int nrmf_rank_combine_s(int64_t n_global, int world, const float *values, float 
 /* tree (size P2c/world), one ncclAllGather of one scalar per rank follows,   */
 /* and every rank evaluates the top levels, so *frob is bitwise identical on  */
 /* every rank and equal to nrmf_cols_[ds]'s frob on one GPU.  Collective when */
-/* frob is non-null.  flags: 0 or NRMF_TOP_CR.  world a power of two.         */
+/* frob is non-null.  flags: NRMF_TOP_CR | NRMF_WS_CLEAN or 0.  world a      */
+/* power of two.                                                             */
 /* ------------------------------------------------------------------------ */
 int nrmf_cols_dist_shard(int64_t cols_global, int world, int rank, int64_t *col_offset, int64_t *col_count);
 size_t nrmf_cols_dist_workspace_bytes(int64_t rows, int64_t cols_global, int world, int elem_bytes);

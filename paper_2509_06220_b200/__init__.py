@@ -30,6 +30,7 @@ LIB_PATH = os.path.join(_HERE, "libnrmf.so")
 
 NRMF_OK = 0
 NRMF_TOP_CR = 1   # include/nrmf.h: cr_hypot above the tile level (A-style final reduction)
+NRMF_WS_CLEAN = 2  # include/nrmf.h: the workspace's counters are known to be zero (no memset)
 _lib = None
 _lock = threading.Lock()
 
@@ -166,11 +167,19 @@ def clear_workspaces():
 
 
 def _flags(top: str) -> int:
+    """Flags of a call: the top-level hypot, and NRMF_WS_CLEAN inside capture():
+    a captured call's arena workspaces are zero-filled once and used only by
+    that call (its warm-up runs and the graph's replays), so the library may
+    skip the per-call counter memset -- the captured call is one kernel."""
     if top == "v1":
-        return 0
-    if top == "cr":
-        return NRMF_TOP_CR
-    raise ValueError(f"nrmf: top must be 'v1' or 'cr', got {top!r}")
+        f = 0
+    elif top == "cr":
+        f = NRMF_TOP_CR
+    else:
+        raise ValueError(f"nrmf: top must be 'v1' or 'cr', got {top!r}")
+    if getattr(_arena, "tensors", None) is not None:
+        f |= NRMF_WS_CLEAN
+    return f
 
 
 def _elem(dtype) -> tuple[int, str]:
@@ -527,7 +536,7 @@ def cols_dist(A_local: torch.Tensor, cols_global: int, group=None, comm: Comm | 
     return (col, fr) if frob else col
 
 
-def capture(fn, warmup: int = 1) -> "torch.cuda.CUDAGraph":
+def capture(fn, warmup: int = 1, graph: "torch.cuda.CUDAGraph | None" = None) -> "torch.cuda.CUDAGraph":
     """Capture one stream-ordered nrmf call (``norm`` / ``cols`` / ``dist`` on
     fixed tensors, e.g. ``lambda: nrmf.dist(x, n, comm=c, out=o)``) in a CUDA
     graph; ``g.replay()`` then re-runs its launches -- counter memset, tree
@@ -536,8 +545,11 @@ def capture(fn, warmup: int = 1) -> "torch.cuda.CUDAGraph":
     the capture stream with workspaces from an arena of its own, which the
     capture reuses and the returned graph keeps alive (``g._nrmf_ws``): no
     other graph or direct call shares them, and clear_workspaces() does not
-    free them.  Replays give the same bits as direct calls (tested); replays
-    of one graph must not overlap each other."""
+    free them.  Captured calls pass NRMF_WS_CLEAN (the arena is zero-filled
+    and dedicated), so a captured norm/cols/dist_p2p call is ONE kernel node.
+    Replays give the same bits as direct calls (tested); replays of one graph
+    must not overlap each other.  `graph`: a CUDAGraph to capture into (e.g.
+    with debug mode enabled)."""
     cs = torch.cuda.Stream()
     cs.wait_stream(torch.cuda.current_stream())
     arena: dict = {}
@@ -549,7 +561,7 @@ def capture(fn, warmup: int = 1) -> "torch.cuda.CUDAGraph":
                 _arena.counts = {}
                 fn()
         torch.cuda.current_stream().wait_stream(cs)
-        g = torch.cuda.CUDAGraph()
+        g = graph if graph is not None else torch.cuda.CUDAGraph()
         _arena.counts = {}
         with torch.cuda.graph(g, stream=cs):
             fn()

@@ -1148,7 +1148,10 @@ static int g_gap_stream = 1;     // test hook: gapped column blocks on the strea
 template <typename F>
 static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int64_t len, int64_t p2,
                        F* tile_out, F* out, int combine, void* ws, size_t ws_bytes, bool vec,
-                       cudaStream_t s, int top_cr, const RankExchange* rx = nullptr) {
+                       cudaStream_t s, int flags, const RankExchange* rx = nullptr) {
+  const int top_cr = flags & NRMF_TOP_CR;
+  // NRMF_WS_CLEAN: the caller guarantees the arrival counters are zero (nrmf.h)
+  const bool clean = (flags & NRMF_WS_CLEAN) != 0;
   if (n_items == 0) return NRMF_OK;
   if (n_items >= (int64_t(1) << 31) - 64) return NRMF_EINVAL;  // kernels index tiles/groups in 32 bits (n < 2^43)
   // contiguous tiles (a vector, or whole columns of T-multiple length stored
@@ -1177,7 +1180,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
       const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
       const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
       if (combine && ws_bytes < need) return NRMF_EWORKSPACE;
-      if (combine && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
+      if (combine && !clean && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
         return NRMF_ECUDA;
       TreeJob<F> job = make_job(x, n_items, tpc, ld, len, tile_out, out, combine, top_cr, ws, cnt_bytes, pl);
       set_exchange(job, rx);
@@ -1234,8 +1237,10 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   if (combine && ws_bytes < need) return NRMF_EWORKSPACE;
   // counters start at zero on every call, whatever the workspace last held
   // (the last arrivers also leave them zero; this makes reuse of one
-  // workspace across calls of different shapes or functions safe)
-  if (combine && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
+  // workspace across calls of different shapes or functions safe) -- unless
+  // the caller vouches for them (NRMF_WS_CLEAN: a workspace dedicated to one
+  // call shape, e.g. a captured graph's; the call is then one kernel)
+  if (combine && !clean && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
     return NRMF_ECUDA;
   TreeJob<F> job = make_job(x, n_items, tpc, ld, len, tile_out, out, combine, top_cr, ws, cnt_bytes, pl);
   set_exchange(job, rx);
@@ -1261,7 +1266,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
 
 template <typename F>
 int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_bytes, cudaStream_t s,
-              int top_cr, const RankExchange* rx) {
+              int flags, const RankExchange* rx) {
   // Evaluate the balanced tree over p2 tiles (p2 >= ceil(n/T), power of two)
   // of x[0..n) padded with +0; *out = root.  Caller validated arguments.
   const int64_t nt = (n + kTile - 1) / kTile;
@@ -1270,7 +1275,7 @@ int tree_eval(int64_t n, const F* x, int64_t p2, F* out, void* ws, size_t ws_byt
     return NRMF_OK;
   }
   const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
-  return launch_tree<F>(x, nt, nt, 0, n, p2, nullptr, out, 1, ws, ws_bytes, vec, s, top_cr, rx);
+  return launch_tree<F>(x, nt, nt, 0, n, p2, nullptr, out, 1, ws, ws_bytes, vec, s, flags, rx);
 }
 
 template int tree_eval<double>(int64_t, const double*, int64_t, double*, void*, size_t, cudaStream_t, int,
@@ -1297,7 +1302,7 @@ static int nrmf_vec(int64_t n, const F* x, F* out, int flags, void* ws, size_t w
     return NRMF_EALIGN;
   const int64_t nt = (n + kTile - 1) / kTile;
   return tree_eval<F>(n, x, pow2_ceil(std::max<int64_t>(nt, 1)), out, ws, ws_bytes,
-                      static_cast<cudaStream_t>(stream), flags & NRMF_TOP_CR);
+                      static_cast<cudaStream_t>(stream), flags);
 }
 
 // ---------------------------------------------------------------- columns
@@ -1342,14 +1347,15 @@ static int nrmf_cols_impl(int64_t rows, int64_t cols, int64_t ld, const F* A, F*
   const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && ((ld * (int64_t)sizeof(F)) & 15) == 0;
   if (tpc == 1)
     return launch_tree<F>(A, cols, 1, ld, rows, p2cols, col_norms, frob, frob != nullptr ? 1 : 0, ws, ws_bytes,
-                          vec, s, cr);
+                          vec, s, flags);
   unsigned* ticket = reinterpret_cast<unsigned*>(ws);
   char* base = static_cast<char*>(ws) + 256;
   F* vals = reinterpret_cast<F*>(base);
   F* partials = reinterpret_cast<F*>(base + align_up((size_t)(cols * tpc) * sizeof(F), 256));
   int st = launch_tree<F>(A, cols * tpc, tpc, ld, rows, 1, vals, nullptr, 0, ws, ws_bytes, vec, s, cr);
   if (st != NRMF_OK) return st;
-  if (frob != nullptr && cudaMemsetAsync(ticket, 0, sizeof(unsigned), s) != cudaSuccess) return NRMF_ECUDA;
+  if (frob != nullptr && !(flags & NRMF_WS_CLEAN) && cudaMemsetAsync(ticket, 0, sizeof(unsigned), s) != cudaSuccess)
+    return NRMF_ECUDA;
   const int64_t nblk = (cols + kAuxThreads - 1) / kAuxThreads;
   cols_combine_kernel<F><<<(unsigned)nblk, kAuxThreads, 0, s>>>(vals, cols, tpc, pow2_ceil(tpc), col_norms,
                                                             p2cols, partials, ticket, frob, cr);
@@ -1513,7 +1519,7 @@ size_t nrmf_workspace_bytes(int64_t n, int elem_bytes) {
   return tree_ws_bytes(nt, pow2_ceil(nt), (size_t)elem_bytes);
 }
 
-static bool flags_ok(int flags) { return (flags & ~NRMF_TOP_CR) == 0; }
+static bool flags_ok(int flags) { return (flags & ~(NRMF_TOP_CR | NRMF_WS_CLEAN)) == 0; }
 
 int nrmf_d(int64_t n, const double* x, double* out, void* ws, size_t ws_bytes, void* stream) {
   return nrmf_vec<double>(n, x, out, 0, ws, ws_bytes, stream);

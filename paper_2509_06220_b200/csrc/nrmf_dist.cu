@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(32) p2p_exchange_kernel(const F* local, PeerAr
 template <typename F>
 int local_step(int64_t n, int world, int rank, int64_t offset, int64_t count, const F* x, F* local, int flags,
                void* ws, size_t ws_bytes, cudaStream_t s, const RankExchange* rx) {
-  if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
+  if ((flags & ~(NRMF_TOP_CR | NRMF_WS_CLEAN)) != 0) return NRMF_EINVAL;
   const int cr = flags & NRMF_TOP_CR;
   if (local == nullptr || ws == nullptr || n < 0 || world < 1 || rank < 0 || rank >= world) return NRMF_EINVAL;
   if (count > 0 && x == nullptr) return NRMF_EINVAL;
@@ -151,7 +151,7 @@ int local_step(int64_t n, int world, int rank, int64_t offset, int64_t count, co
   const int64_t P2 = pow2_ceil(std::max<int64_t>(nt, 1));
   const int64_t p2ws = world <= P2 ? P2 / world : 1;
   const size_t tws = tree_workspace(p2ws, sizeof(F));
-  if (p2l > 0 && cnt > 0) return tree_eval<F>(cnt, x, p2l, local, ws, tws, s, cr, rx);
+  if (p2l > 0 && cnt > 0) return tree_eval<F>(cnt, x, p2l, local, ws, tws, s, flags, rx);
   // no data here: the subtree value is +0
   F* zero = reinterpret_cast<F*>(static_cast<char*>(ws) + tws);
   if (cudaMemsetAsync(rx ? zero : local, 0, sizeof(F), s) != cudaSuccess) return NRMF_ECUDA;
@@ -166,7 +166,7 @@ int local_step(int64_t n, int world, int rank, int64_t offset, int64_t count, co
 // P:1077-1084).
 template <typename F>
 int rank_combine(int64_t n, int world, const F* values, F* out, int flags, cudaStream_t s) {
-  if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
+  if ((flags & ~(NRMF_TOP_CR | NRMF_WS_CLEAN)) != 0) return NRMF_EINVAL;
   if (values == nullptr || out == nullptr || n < 0 || world < 1) return NRMF_EINVAL;
   if (reinterpret_cast<uintptr_t>(values) % sizeof(F) || reinterpret_cast<uintptr_t>(out) % sizeof(F))
     return NRMF_EALIGN;
@@ -266,7 +266,7 @@ size_t cols_dist_ws(int64_t rows, int64_t cols, int world, size_t esz) {
 template <typename F>
 int cols_dist_impl(int64_t rows, int64_t cols, int64_t ld, int64_t col_off, int64_t col_cnt, const F* A,
                    F* col_norms, F* frob, int flags, void* ws, size_t ws_bytes, void* comm_v, void* stream) {
-  if ((flags & ~NRMF_TOP_CR) != 0) return NRMF_EINVAL;
+  if ((flags & ~(NRMF_TOP_CR | NRMF_WS_CLEAN)) != 0) return NRMF_EINVAL;
   const int cr = flags & NRMF_TOP_CR;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (rows < 0 || cols < 0 || ld < rows || col_off < 0 || col_cnt < 0) return NRMF_EINVAL;

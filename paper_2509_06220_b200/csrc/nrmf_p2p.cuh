@@ -7,14 +7,19 @@
 // launch.
 //
 // Peer buffer (kP2PBytes, one per rank, zero-filled once): two parity halves
-// (epoch & 1) of [flags: kP2PMaxRanks x u32][values: kP2PMaxRanks x 8 B], and
-// the rank's call counter (epoch) at kP2PEpochOff.  Call e writes half e&1; a
-// rank can only reach call e+2 after finishing call e+1, which needs every
-// rank's e+1 flag, which a rank writes only after it has finished reading call
-// e -- so a half is never overwritten while read.  The epoch lives in device
-// memory and is advanced by the exchange itself (1, 2, 3, ... on every rank,
-// since every rank makes the same calls), so a call can be captured in a CUDA
-// graph and replayed.
+// (epoch & 1) of kP2PMaxRanks 16-byte slots, and the rank's call counter
+// (epoch) at kP2PEpochOff.  Slot r of rank p's buffer receives rank r's value
+// for call e as {lo32, e, hi32, e}: each aligned 8-byte half carries the
+// epoch beside its 32 data bits and is stored and loaded as one unit (the
+// "LL" flag-in-data idea NCCL uses for small messages), so a reader that sees
+// epoch e in both halves has the whole value -- no system-scope fence on
+// either side (a release/acquire pair across GPUs costs microseconds).  Call
+// e writes half e&1; a rank can only reach call e+2 after finishing call e+1,
+// which needs every rank's e+1 value, which a rank writes only after it has
+// finished reading call e -- so a half is never overwritten while read.  The
+// epoch lives in device memory and is advanced by the exchange itself (1, 2,
+// 3, ... on every rank, since every rank makes the same calls), so a call can
+// be captured in a CUDA graph and replayed.
 #pragma once
 
 #include <cstdint>
@@ -24,25 +29,39 @@
 namespace nrmf {
 
 constexpr int kP2PMaxRanks = 32;
-constexpr int kP2PHalf = kP2PMaxRanks * 4 + kP2PMaxRanks * 8;  // 384 B
+constexpr int kP2PSlot = 16;
+constexpr int kP2PHalf = kP2PMaxRanks * kP2PSlot;  // 512 B
 constexpr int kP2PEpochOff = 2 * kP2PHalf;
-constexpr int kP2PBytes = 1024;
+constexpr int kP2PBytes = 1280;
 static_assert(kP2PEpochOff + 4 <= kP2PBytes, "p2p buffer");
 
 struct PeerArgs {
   char* const* peers;  // device array: peers[r] = rank r's buffer as mapped here (peers[rank] = own)
   int world;           // <= kP2PMaxRanks
   int rank;
-  unsigned* err;       // nullable: set to 1 if a flag did not arrive in time
+  unsigned* err;       // nullable: set to 1 if a value did not arrive in time
 };
 
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_ll(char* p, uint32_t lo, uint32_t hi, uint32_t e) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(lo), "r"(e), "r"(hi), "r"(e)
+               : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+__device__ __forceinline__ void ld_ll(const char* p, uint32_t& lo, uint32_t& e0, uint32_t& hi, uint32_t& e1) {
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(lo), "=r"(e0), "=r"(hi), "=r"(e1)
+               : "l"(p) : "memory");
+}
+__device__ __forceinline__ void to_words(double v, uint32_t& lo, uint32_t& hi) {
+  lo = (uint32_t)__double2loint(v);
+  hi = (uint32_t)__double2hiint(v);
+}
+__device__ __forceinline__ void to_words(float v, uint32_t& lo, uint32_t& hi) {
+  lo = __float_as_uint(v);
+  hi = 0u;
+}
+template <typename F>
+__device__ __forceinline__ F from_words(uint32_t lo, uint32_t hi) {
+  if constexpr (sizeof(F) == 8) return __hiloint2double((int)hi, (int)lo);
+  else return __uint_as_float(lo);
 }
 
 // Warp-collective (all 32 lanes).  Returns, in every lane, the balanced tree
@@ -54,27 +73,26 @@ __device__ F rank_exchange(F local, const PeerArgs& a, int nr, int cr) {
   unsigned* const own_epoch = reinterpret_cast<unsigned*>(a.peers[a.rank] + kP2PEpochOff);
   const uint32_t epoch = *reinterpret_cast<volatile unsigned*>(own_epoch) + 1u;
   const uint32_t half = (epoch & 1u) * kP2PHalf;
-  if (lane < a.world) {  // lane p publishes this rank's value in peer p's buffer
-    char* pb = a.peers[lane] + half;
-    volatile F* slot = reinterpret_cast<volatile F*>(pb + kP2PMaxRanks * 4 + a.rank * 8);
-    *slot = local;
-    __threadfence_system();  // the value is visible before the flag
-    st_release_sys(reinterpret_cast<unsigned*>(pb) + a.rank, epoch);
-  }
+  uint32_t wlo, whi;
+  to_words(local, wlo, whi);
+  if (lane < a.world)  // lane p publishes this rank's value in peer p's buffer
+    st_ll(a.peers[lane] + half + a.rank * kP2PSlot, wlo, whi, epoch);
   F v = F(0);
   if (lane < a.world) {  // lane r waits for rank r's value in this rank's buffer
-    const char* own = a.peers[a.rank] + half;
-    const unsigned* flag = reinterpret_cast<const unsigned*>(own) + lane;
+    const char* slot = a.peers[a.rank] + half + lane * kP2PSlot;
+    uint32_t lo, e0, hi, e1;
     bool ok = true;
-    for (long long spins = 0; ld_acquire_sys(flag) != epoch; ++spins) {
+    for (long long spins = 0;; ++spins) {
+      ld_ll(slot, lo, e0, hi, e1);
+      if (e0 == epoch && e1 == epoch) break;
       if (spins > (1ll << 24)) {  // ~ seconds: a rank did not call; report, do not hang
         ok = false;
         break;
       }
-      __nanosleep(128);
+      if (spins > 64) __nanosleep(64);
     }
     if (ok) {
-      v = *reinterpret_cast<const volatile F*>(own + kP2PMaxRanks * 4 + lane * 8);
+      v = from_words<F>(lo, hi);
     } else {
       v = sizeof(F) == 8 ? F(__longlong_as_double(0x7ff8000000000000ll)) : F(__int_as_float(0x7fc00000));
       if (a.err != nullptr) atomicExch(a.err, 1u);

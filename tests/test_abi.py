@@ -86,7 +86,7 @@ def test_workspace_alignment_is_checked_at_enqueue(L):
     assert L.nrmf_dist_local_d(10, 2, 0, 0, 9, 16, 16, 0, 1024, big, None) == 4       # not the canonical shard
     assert L.nrmf_dist_local_d(10, 3, 0, 0, 10, 16, 16, 0, 1024, big, None) == 4      # world not a power of two
     assert L.nrmf_rank_combine_d(10, 2, 12, 16, 0, None) == 2                          # values misaligned
-    assert L.nrmf_rank_combine_d(10, 2, 16, 16, 2, None) == 1                          # unknown flag
+    assert L.nrmf_rank_combine_d(10, 2, 16, 16, 4, None) == 1                          # unknown flag
 
 
 @pytest.mark.parametrize("n,G", [(1 << 30, 1), (1 << 30, 2), (1 << 30, 8), (5, 8), (4097, 4),
