@@ -314,6 +314,90 @@ __global__ void check_edges_s(uint64_t seed, uint64_t n, Counts* c) {
   atomicAdd(&c->checked, ck); atomicAdd(&c->fast, fa); atomicAdd(&c->mism, mi);
 }
 
+// Safe node (v1h_safe_n, the tile fallback) against the IEEE-intrinsic node
+// on EVERY kind of operand: full exponent range incl. subnormals, +-0, +-inf,
+// NaN, huge values near DBL_MAX / FLT_MAX (overflow of h), q near 1, tiny q,
+// and M at the edges of the scaling ranges.  Every pair must match (NaN: both
+// NaN).  Packed pairs (N = 2, 4) too.
+__device__ double special_d(uint64_t k) {
+  switch (k % 16) {
+    case 0: return 0.0;
+    case 1: return __longlong_as_double(0x7ff0000000000000ll);                         // +inf
+    case 2: return __longlong_as_double(0x7ff8000000000000ll | (long long)(k >> 40));    // NaN
+    case 3: return __longlong_as_double((long long)(mix(k) & ((1ull << 52) - 1)));      // subnormal
+    case 4: return 1.7976931348623157e308 * (1.0 - (double)(mix(k) % 1024) * 0x1p-53);   // near DBL_MAX
+    case 5: return __longlong_as_double(0x07b0000000000000ll + (long long)(mix(k) % 129) - 64);  // ~2^-900
+    case 6: return __longlong_as_double(0x7fc0000000000000ll + (long long)(mix(k) % 129) - 64);  // ~2^1021
+    case 7: return 0x1p-1022 * (1.0 + (double)(mix(k) >> 12) * 0x1p-52);
+    default: return gen_d(k, 0);
+  }
+}
+__global__ void check_safe_d(uint64_t seed, uint64_t n, Counts* c) {
+  unsigned long long ck = 0, mi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    double x = special_d(k);
+    double y;
+    if (mix(k + 11) & 1) y = special_d(mix(k + 3));
+    else y = __dmul_rn(x, 1.0 - (double)(mix(k + 5) >> 12) * 0x1p-53 * (double)(mix(k + 6) % 4));  // q near 1
+    if (k & (1ull << 30)) x = -x;
+    if (k & (1ull << 31)) y = -y;
+    const double a[4] = {x, y, -x, y}, b[4] = {y, x, y, -x};
+    double h[4], h1[1];
+    v1h_safe_n<4>(a, b, h);
+    const double a1[1] = {x}, b1[1] = {y};
+    v1h_safe_n<1>(a1, b1, h1);
+    const double e = v1h(x, y);
+    ++ck;
+    for (int j = 0; j < 5; ++j) {
+      const double g = j < 4 ? h[j] : h1[0];
+      const bool same = (g != g && e != e) || __double_as_longlong(g) == __double_as_longlong(e);
+      if (!same) ++mi;
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
+}
+__device__ float special_s(uint64_t k) {
+  switch (k % 16) {
+    case 0: return 0.0f;
+    case 1: return __int_as_float(0x7f800000);
+    case 2: return __int_as_float(0x7fc00000 | (int)((k >> 40) & 0x3fffff));
+    case 3: return __int_as_float((int)(mix(k) & ((1u << 23) - 1)));
+    case 4: return 3.4028234663852886e38f * (1.0f - (float)(mix(k) % 64) * 0x1p-24f);
+    case 5: return __int_as_float(0x17800000 + (int)(mix(k) % 129) - 64);   // ~2^-80
+    case 6: return __int_as_float(0x7e000000 + (int)(mix(k) % 129) - 64);   // ~2^125
+    default: {
+      const int e1 = (int)(mix(k) % 277) - 149;
+      return ldexpf(1.0f + (float)(k >> 41) * 0x1p-23f, e1);
+    }
+  }
+}
+__global__ void check_safe_s(uint64_t seed, uint64_t n, Counts* c) {
+  unsigned long long ck = 0, mi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(seed ^ (i * 2 + 1));
+    float x = special_s(k);
+    float y;
+    if (mix(k + 11) & 1) y = special_s(mix(k + 3));
+    else y = __fmul_rn(x, 1.0f - (float)(mix(k + 5) % 64) * 0x1p-24f);
+    if (k & (1ull << 30)) x = -x;
+    if (k & (1ull << 31)) y = -y;
+    const float a[4] = {x, y, -x, y}, b[4] = {y, x, y, -x};
+    float h[4], h1[1];
+    v1h_safe_n<4>(a, b, h);
+    const float a1[1] = {x}, b1[1] = {y};
+    v1h_safe_n<1>(a1, b1, h1);
+    const float e = v1h(x, y);
+    ++ck;
+    for (int j = 0; j < 5; ++j) {
+      const float g = j < 4 ? h[j] : h1[0];
+      const bool same = (g != g && e != e) || __float_as_int(g) == __float_as_int(e);
+      if (!same) ++mi;
+    }
+  }
+  atomicAdd(&c->checked, ck); atomicAdd(&c->mism, mi);
+}
+
 extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long n, int mode,
                          unsigned long long* out3) {
   Counts* c;
@@ -330,6 +414,8 @@ extern "C" int fastcheck(int which, unsigned long long seed, unsigned long long 
     case 7: check_div_d_midpoints<<<148 * 8, 256>>>(seed, n, c); break;
     case 8: check_edges_d<<<148 * 8, 256>>>(seed, n, c); break;
     case 9: check_edges_s<<<148 * 8, 256>>>(seed, n, c); break;
+    case 10: check_safe_d<<<148 * 8, 256>>>(seed, n, c); break;
+    case 11: check_safe_s<<<148 * 8, 256>>>(seed, n, c); break;
     default: return 2;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return 3;

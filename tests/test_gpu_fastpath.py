@@ -99,3 +99,14 @@ def test_fast_domain_edges(fc, which):
     unflagged leaf nodes and in-domain internal nodes equal the exact node."""
     checked, fast, mism = fc(which, seed=91 + which, n=1 << 26)
     assert checked == 1 << 26 and mism == 0 and fast > 0
+
+
+@pytest.mark.parametrize("which", [10, 11], ids=["fp64", "fp32"])
+def test_safe_node_equals_exact_node_everywhere(fc, which):
+    """The safe node (v1h_safe_n: the fast sequences on power-of-two-scaled
+    operands, the tile fallback) equals the IEEE-intrinsic node of Listing 2
+    for every kind of operand: full range incl. subnormals, +-0, +-inf, NaN,
+    values near the format's maximum (h overflows), q near 1, M at the edges
+    of the scaling ranges; scalar and packed (4 chains) forms."""
+    checked, _, mism = fc(which, seed=101 + which, n=1 << 28)
+    assert checked == 1 << 28 and mism == 0

@@ -103,7 +103,8 @@ def test_dist_p2p_world1(nrmf, grid):
 
 def test_dist_p2p_graph_replay_world1(nrmf):
     """The exchange keeps its call counter in device memory: a captured
-    dist_p2p call replays correctly (here on a 1-rank group)."""
+    dist_p2p call is one kernel node and replays correctly (here on a 1-rank
+    group)."""
     import torch.distributed as td
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29549")
@@ -118,7 +119,13 @@ def test_dist_p2p_graph_replay_world1(nrmf):
         xh = gen.normal(5, n, dtype=np.float64)
         x = torch.from_numpy(xh).cuda()
         out = torch.empty((), dtype=torch.float64, device="cuda")
-        g = nrmf.capture(lambda: nrmf.dist_p2p(x, n, pg, out=out))
+        g = torch.cuda.CUDAGraph(keep_graph=True)
+        nrmf.capture(lambda: nrmf.dist_p2p(x, n, pg, out=out), graph=g)
+        # the whole distributed step is ONE kernel: no counter memset
+        # (NRMF_WS_CLEAN in capture), the exchange inside the tree kernel
+        from test_gpu_graph import _graph_node_types
+        assert _graph_node_types(g) == ["cudaGraphNodeTypeKernel"]
+        g.instantiate()
         for _ in range(4):
             g.replay()
             torch.cuda.synchronize()
