@@ -39,6 +39,9 @@ constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's l
 #ifndef NRMF_USE_TMA
 #define NRMF_USE_TMA 1        // 0: aligned full tiles use direct LDG.128 instead of the TMA ring
 #endif
+#ifndef NRMF_SKIP_FLAGGED
+#define NRMF_SKIP_FLAGGED 1   // stream kernel: stop evaluating a group at its first flagged tile
+#endif
 #ifndef NRMF_CTA_STEP
 #define NRMF_CTA_STEP 1       // stream kernel: first combine step (16 warp groups) inside the CTA
 #endif
@@ -67,6 +70,22 @@ __device__ __forceinline__ void trace(unsigned type, unsigned level, unsigned id
 #define NRMF_TRACE(a, b, c) trace(a, b, c)
 #else
 #define NRMF_TRACE(a, b, c) (void)0
+#endif
+
+#ifdef NRMF_PROBE_JITTER  // test build only: random delays at every step of the combine protocols
+__device__ __forceinline__ void jitter(unsigned salt) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  unsigned h = (unsigned)(t ^ (t >> 17)) * 0x9E3779B1u ^ (salt * 0x85EBCA6Bu) ^ (blockIdx.x * 0xC2B2AE35u) ^
+               (threadIdx.x >> 5);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3) != 0) __nanosleep(h % 4000u);  // 0 .. 4 us, three times in four
+}
+#define NRMF_JITTER(s) jitter(s)
+#else
+#define NRMF_JITTER(s) (void)0
 #endif
 
 // One evaluation of the tile tree.  Work unit of a warp: a "warp group" of
@@ -238,6 +257,7 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != expect - 1) return;
     NRMF_TRACE(2, k, 0);
+    NRMF_JITTER(3);
     if (lane == 0) {
       // acquire by the lane that read the counter: the other arrivals' values
       // (released by their atomics) are visible to it ...
@@ -251,8 +271,10 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
       write_root(job, v);
       return;
     }
+    NRMF_JITTER(1);
     if (lane == 0) {
       job.vals[job.val_off[k + 1] + g] = v;
+      NRMF_JITTER(2);
       old = atom_add_release(job.cnt + job.cnt_off[k + 1] + (g >> job.lg_fan[k + 1]), 1u);
     }
     ++k;
@@ -472,6 +494,13 @@ struct StreamLoader {
   __device__ __forceinline__ void begin(int) {
     mbar_wait(my_s + L::kBars + (consumed % kStages) * 8, (consumed / kStages) & 1);
   }
+  // consume `nb` batches without reading them (the ring keeps streaming)
+  __device__ __noinline__ void drain(int nb) {
+    for (int i = 0; i < nb; ++i) {
+      begin(i);
+      end(i);
+    }
+  }
   __device__ __forceinline__ void get_row(int, int row, F (&o)[Cfg<F>::V]) const {
 #ifdef NRMF_FAKE_SMEM  // dev-only energy/timing probe: leaves synthesized in registers (wrong results)
 #pragma unroll
@@ -554,8 +583,11 @@ __device__ void cta_try(const TreeJob<F>& job, uint32_t cta_s, int rr, int b, in
   const uint32_t cs = cta_s + C::kCnt + slot * 4, ts = cta_s + C::kTag + slot * 4;
   const int expect = n_groups - 16 * b < 16 ? n_groups - 16 * b : 16;
   unsigned got = 0;
-  if (lane == 0 && ld_volatile_shared_u32(ts) == (unsigned)rr && ld_volatile_shared_u32(cs) == (unsigned)expect)
+  NRMF_JITTER(4);
+  if (lane == 0 && ld_volatile_shared_u32(ts) == (unsigned)rr && ld_volatile_shared_u32(cs) == (unsigned)expect) {
+    NRMF_JITTER(5);
     got = cas_acq_rel_cta_shared(ts, (unsigned)rr, (unsigned)rr | kClaimed) == (unsigned)rr;
+  }
   if (!__shfl_sync(0xffffffffu, got, 0)) return;
   // lane 0 read the complete count (written by the arrivals' release adds):
   // its fence makes every arrival's value visible to it, and __syncwarp
@@ -575,6 +607,7 @@ __device__ void cta_try(const TreeJob<F>& job, uint32_t cta_s, int rr, int b, in
   if (bad)
     for (int l = 0; l < 4; ++l) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), job.top_cr);
   __syncwarp();
+  NRMF_JITTER(6);
   if (lane == 0) {  // free the slot for round rr + kCtaSlots (its values are read)
     st_shared_u32(cs, 0u);
     fence_acq_rel_cta();
@@ -607,10 +640,13 @@ __device__ __forceinline__ void cta_arrive(const TreeJob<F>& job, uint32_t cta_s
     // acquire orders this round's value store and count after the claimer's
     // reads and counter reset
     while (ld_acquire_cta_shared_u32(ts) != (unsigned)r) __nanosleep(64);
+    NRMF_JITTER(7);
     st_shared(cta_s + C::kVals + (slot * 16 + (grp & 15)) * (uint32_t)sizeof(F), gv);
+    NRMF_JITTER(8);
     red_add_release_cta_shared(cta_s + C::kCnt + slot * 4, 1u);
   }
   __syncwarp();
+  NRMF_JITTER(9);
   const int b = grp >> 4;
   if (r >= 1) cta_try<F>(job, cta_s, r - 1, b - W / 16, n_groups);
   if (grp + W >= n_groups) cta_try<F>(job, cta_s, r, b, n_groups);
@@ -728,6 +764,14 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
       for (int k = 0; k < G; ++k) {  // rolled
         const F c = warp_tile_lanes<F>(sl, node, sl.my_s + WarpSmem<F>::kStash);
         st_shared(sl.my_s + WarpSmem<F>::kXs + (k * 32 + lane) * (uint32_t)sizeof(F), c);
+#if NRMF_SKIP_FLAGGED
+        // a flagged tile sends the whole group to the fallback: the group's
+        // remaining batches are only drained from the ring, not evaluated
+        if (k + 1 < G && __any_sync(0xffffffffu, node.bad)) {
+          sl.drain((G - 1 - k) * (Cfg<F>::J / kBatch));
+          break;
+        }
+#endif
       }
       __syncwarp();
 #ifdef NRMF_PROBE_NO_GROUPCROSS  // dev-only timing probe: no cross-thread/group levels (wrong results)
@@ -821,6 +865,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     }
     // announce this warp group; the last arriver of its 2^lg_fan group climbs.
     unsigned old = 0;
+    NRMF_JITTER(10);
     if (lane == 0) {
       job.vals[job.val_off[0] + grp] = gv[0];
       old = atom_add_release(job.cnt + job.cnt_off[0] + (grp >> job.lg_fan[0]), 1u);
@@ -912,6 +957,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     return;
   }
   unsigned old = 0;
+  NRMF_JITTER(11);
   if (lane == 0) {
     job.vals[job.val_off[0] + grp] = gv;
     old = atom_add_release(job.cnt + job.cnt_off[0] + (grp >> job.lg_fan[0]), 1u);
