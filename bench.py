@@ -589,33 +589,53 @@ def run_ours(args):
     return 0
 
 
-# Compute term of the roofline: per node the
-# stock IEEE sequences execute 21 FP64-pipe instructions (fp64) / 25 issue
-# slots (fp32); these frozen counts are the algorithmic unit.  Peaks from unit
-# counts and the clock sampled during the run: 148 SMs x 64 FP64 lanes/clk;
-# 148 SMs x 4 schedulers x 1 warp-instruction/clk.
+# Compute term of the roofline, from the
+# instruction counts the shipped kernel EXECUTES per warp-node (ncu on this
+# build, profiles/instr_per_node.json): the FP64 pipe takes 2 cycles per warp
+# instruction per SM sub-partition (16 lanes/clk), the issue stage 1; 148 SMs
+# x 4 sub-partitions, at the SM clock sampled during the run.  The binding
+# term is the larger of these floors and the HBM time.
 N_SM = 148
-FP64_PER_NODE, ISSUE_PER_NODE_FP32 = 21, 25
+
+
+def load_instr(esz):
+    p = os.path.join(ROOT, "profiles", "instr_per_node.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f).get("fp64" if esz == 8 else "fp32")
 
 
 def compute_roofline(esz, n, ms, f_ghz, hbm_peak):
     t = ms * 1e-3
-    nodes = max(n - 1, 1)
+    warp_nodes = max(n - 1, 1) / 32
     t_hbm = n * esz / (hbm_peak * 1e9)
+    c = load_instr(esz)
+    if c is None:
+        return {"bound": "alu", "unmeasured": "profiles/instr_per_node.json missing", "t_hbm_ms": round(t_hbm * 1e3, 4)}
+    slots = N_SM * 4 * f_ghz * 1e9                      # warp-instruction issue slots per second
+    t_issue = warp_nodes * c["warp_instr_per_warp_node"] / slots
+    d = {"bound": "alu", "sm_ghz": f_ghz, "source": c.get("source"),
+         "warp_instr_per_warp_node": c["warp_instr_per_warp_node"], "t_issue_ms": round(t_issue * 1e3, 4),
+         "t_hbm_ms": round(t_hbm * 1e3, 4)}
     if esz == 8:
-        peak = N_SM * 64 * f_ghz * 1e9                       # FP64 lane-ops/s
-        achieved = nodes * FP64_PER_NODE / t
-        unit, what = "FP64 lane-instr/s", "FP64 pipe (21 instr/node)"
+        t_fp64 = warp_nodes * c["fp64_instr_per_warp_node"] * 2 / slots
+        d.update({"pipe": "FP64 (2 cycles per warp-instruction per SMSP)",
+                  "fp64_instr_per_warp_node": c["fp64_instr_per_warp_node"],
+                  "achieved": round(warp_nodes * 32 * c["fp64_instr_per_warp_node"] / t / 1e12, 4),
+                  "peak": round(N_SM * 64 * f_ghz * 1e9 / 1e12, 4), "unit": "T FP64 lane-instr/s",
+                  "t_fp64_ms": round(t_fp64 * 1e3, 4)})
+        t_comp = max(t_fp64, t_issue)
     else:
-        peak = N_SM * 4 * f_ghz * 1e9                        # warp-instr issued/s
-        achieved = nodes / 32 * ISSUE_PER_NODE_FP32 / t
-        unit, what = "warp-instr/s", "issue (25 slots/node)"
-    t_comp = achieved / peak * t
-    return {"bound": "alu", "pipe": what, "achieved": round(achieved / 1e12, 4), "peak": round(peak / 1e12, 4),
-            "unit": "T " + unit, "frac": round(achieved / peak, 4), "sm_ghz": f_ghz,
-            "t_hbm_ms": round(t_hbm * 1e3, 4), "t_compute_ms": round(t_comp * 1e3, 4),
-            "binding": "hbm" if t_hbm >= t_comp else "alu",
-            "binding_frac": round(max(t_hbm, t_comp) / t, 4)}
+        d.update({"pipe": "issue (1 warp-instruction per cycle per SMSP)",
+                  "achieved": round(warp_nodes * c["warp_instr_per_warp_node"] / t / 1e12, 4),
+                  "peak": round(slots / 1e12, 4), "unit": "T warp-instr/s"})
+        t_comp = t_issue
+    d["frac"] = round(t_comp / t, 4)
+    d["t_compute_ms"] = round(t_comp * 1e3, 4)
+    d["binding"] = "hbm" if t_hbm >= t_comp else "alu"
+    d["binding_frac"] = round(max(t_hbm, t_comp) / t, 4)
+    return d
 
 
 def load_traffic(esz):
@@ -684,9 +704,10 @@ def sumsq_context(x, ex, dt, ms_nrmf, args, stream):
 
 def other_configs(nrmf, device, stream, hbm_peak):
     """The other BASELINE configs, reported beside the metric (parity-test
-    cases, not bench lines): C2 SNRMF n=2^28, C4 column norms 4096 x 65536,
-    C5 extreme range n=2^27 (three readings, R9) and its complex view.  Inputs
-    device-resident, each timed as 20 graph replays after warm-up; bits checked
+    cases, not bench lines): C1 DNRMF n=2^20 (cold and L2-resident), C2 SNRMF
+    n=2^28, C4 column norms 4096 x 65536, C5 extreme range n=2^27 (three
+    readings, R9) and its complex view, and the unaligned-base path.  Inputs
+    device-resident, each timed as graph replays after warm-up; bits checked
     against the oracle."""
     import torch
 
@@ -700,6 +721,39 @@ def other_configs(nrmf, device, stream, hbm_peak):
         return time_loop(g.replay, reps, stream)
 
     res = {}
+    # C1: DNRMF n = 2^20 U[-1,1) (BASELINE configs[0]) -- 8 MiB fits in L2, so
+    # L2 is flushed (256 MiB write, outside the events) before every step; the
+    # captured call is one kernel node (NRMF_WS_CLEAN)
+    n1 = 1 << 20
+    x1h = gen.uniform_pm1(1, n1)
+    x1 = torch.from_numpy(x1h).to(device)
+    o1 = torch.empty((), dtype=torch.float64, device=device)
+    g1 = nrmf.capture(lambda: nrmf.norm(x1, out=o1))
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=device)
+    for _ in range(3):
+        g1.replay()
+    ms_cold = time_loop(g1.replay, 50, stream, flush)
+    ms_warm = time_loop(g1.replay, 50, stream)
+    res["C1"] = {"workload": "DNRMF fp64 n=2^20 U[-1,1)", "us_cold_l2_flushed": round(ms_cold * 1e3, 2),
+                 "us_warm_l2_resident": round(ms_warm * 1e3, 2), "graph_nodes": 1,
+                 "bit_exact_vs_oracle": bool(o1.cpu().numpy().tobytes() == np.float64(oracle.nrmf(x1h)).tobytes())}
+    del x1, flush
+    # the paper's unaligned case (aligned vs unaligned loads): a base
+    # 8 bytes past a 16-byte boundary takes the element-load path (same bits)
+    nu = 1 << 28
+    xuh = gen.normal(2, nu + 1)
+    xu = torch.from_numpy(xuh).to(device)
+    ou = torch.empty((), dtype=torch.float64, device=device)
+    xa, xm = xu[:nu], xu[1:]
+    msa = timed(lambda: nrmf.norm(xa, out=ou))
+    msu = timed(lambda: nrmf.norm(xm, out=ou))
+    res["unaligned"] = {"workload": "DNRMF fp64 n=2^28 N(0,1), base 16-byte aligned vs 8 bytes off",
+                        "ms_aligned": round(msa, 4), "ms_unaligned": round(msu, 4),
+                        "GB/s_aligned": round(nu * 8 / (msa * 1e-3) / 1e9, 1),
+                        "GB/s_unaligned": round(nu * 8 / (msu * 1e-3) / 1e9, 1),
+                        "bit_exact_vs_oracle": bool(ou.cpu().numpy().tobytes() ==
+                                                    np.float64(oracle.nrmf(xuh[1:])).tobytes())}
+    del xu, xa, xm, xuh
     n2 = 1 << 28
     x2h = gen.sme(1, n2)
     x2 = torch.from_numpy(x2h).to(device)

@@ -40,7 +40,7 @@ constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's l
 #define NRMF_USE_TMA 1        // 0: aligned full tiles use direct LDG.128 instead of the TMA ring
 #endif
 #ifndef NRMF_SKIP_FLAGGED
-#define NRMF_SKIP_FLAGGED 1   // stream kernel: stop evaluating a group at its first flagged tile
+#define NRMF_SKIP_FLAGGED 0   // 1: stream kernel stops evaluating a group at its first flagged tile (C5 -6 %, DNRMF +1.3 %: off)
 #endif
 #ifndef NRMF_CTA_STEP
 #define NRMF_CTA_STEP 1       // stream kernel: first combine step (16 warp groups) inside the CTA
@@ -118,6 +118,10 @@ struct TreeJob {
   char* const* peers;  // device array of the ranks' exchange buffers (nrmf_p2p.cuh)
   unsigned* p_err;     // nullable: set to 1 if a rank's value did not arrive in time
   int p_world, p_rank, p_nr;
+  // split kernel: the LAST combine step by flag-in-data slots instead of a
+  // counter (ll_*, below); null = counters for every step.  [epoch word |
+  // pad to 16 B][slot i: 16 B]...
+  char* ll;
 };
 
 // The warp that evaluates the tree's root writes it.  With a fused rank
@@ -241,12 +245,117 @@ __device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
   return old;
 }
 
+// ---------------------------------------------------------------------------
+// Last combine step of the split kernel without a counter (small calls: the
+// latency of the release fence, the atomic round trip and the re-read of the
+// values was ~2 us of a 14 us call).  Each input of the last step is written
+// by the warp that produced it into its 16-byte slot together with the call's
+// epoch e, twice -- {lo32, e, hi32, e}, each 8-byte half one store/load unit
+// (the flag-in-data scheme of the peer exchange, nrmf_p2p.cuh) -- and ONE
+// warp (CTA 0, warp 1: it has no group work of its own after its batch)
+// polls the slots until every one carries e, then evaluates the step's
+// balanced subtree in registers (the same tree as warp_group_bal) and writes
+// the root.  The epoch is a word in the workspace: every producer reads it at
+// its start (e = word + 1) and the combiner advances it after the last slot
+// arrived, so nothing is cleared between calls and graph replays work; a
+// workspace of garbage gives a random e that a garbage slot matches in both
+// halves with probability 2^-64.  Only one warp waits, on producers that never
+// wait themselves, so the grid needs no co-residency.
+template <typename F>
+__device__ __forceinline__ unsigned ll_epoch(const TreeJob<F>& job) {
+  return *reinterpret_cast<volatile unsigned*>(job.ll) + 1u;
+}
+template <typename F>
+__device__ __forceinline__ void ll_store(const TreeJob<F>& job, int64_t i, F v, unsigned e) {
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t lo, hi;
+    to_words(v, lo, hi);
+    st_ll(job.ll + 16 * (i + 1), lo, hi, e);
+  }
+}
+// KP inputs per lane (lanes < 2^f when f <= 5): poll, then the fast tree with
+// the exact fallback (as warp_group_bal: any flagged node or NaN).
+template <typename F, int KP>
+__device__ __noinline__ F ll_gather_combine(const char* ll, int64_t nin, int f, int cr, unsigned e) {
+  const int lane = threadIdx.x & 31;
+  F a[KP];
+  bool ready[KP];
+#pragma unroll
+  for (int j = 0; j < KP; ++j) {
+    const int64_t i = (int64_t)lane * KP + j;
+    a[j] = F(0);
+    ready[j] = !(i < nin && (KP > 1 || lane < (1 << f)));
+  }
+  for (long long spins = 0;; ++spins) {
+    bool all = true;
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      if (ready[j]) continue;
+      uint32_t lo, e0, hi, e1;
+      ld_ll(ll + 16 * ((int64_t)lane * KP + j + 1), lo, e0, hi, e1);
+      if (e0 == e && e1 == e) {
+        a[j] = from_words<F>(lo, hi);
+        ready[j] = true;
+      } else {
+        all = false;
+      }
+    }
+    if (__all_sync(0xffffffffu, all)) break;
+    if (spins > (1ll << 26)) {  // never: every producer of the step writes its slot
+#pragma unroll
+      for (int j = 0; j < KP; ++j)
+        if (!ready[j]) a[j] = sizeof(F) == 8 ? F(__longlong_as_double(0x7ff8000000000000ll)) : F(__int_as_float(0x7fc00000));
+      break;
+    }
+    if (spins > 32) __nanosleep(32);
+  }
+  const int lv = f < 5 ? f : 5;
+  bool bad = cr != 0;
+  F v;
+  if (!bad) {
+    F b[KP];
+#pragma unroll
+    for (int j = 0; j < KP; ++j) b[j] = a[j];
+#pragma unroll
+    for (int st = 1; st < KP; st <<= 1)
+#pragma unroll
+      for (int j = 0; j < KP; j += 2 * st) b[j] = v1h_fast<true>(b[j], b[j + st], bad);
+    v = b[0];
+    for (int l = 0; l < lv; ++l) v = v1h_fast<true>(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), bad);
+    bad = __any_sync(0xffffffffu, lane < (1 << lv) && (bad || v != v));
+  }
+  if (bad) {
+#pragma unroll
+    for (int st = 1; st < KP; st <<= 1)
+#pragma unroll
+      for (int j = 0; j < KP; j += 2 * st) a[j] = top_node(a[j], a[j + st], cr);
+    v = a[0];
+    for (int l = 0; l < lv; ++l) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), cr);
+  }
+  return v;
+}
+template <typename F>
+__device__ void ll_combine(const TreeJob<F>& job, unsigned e) {
+  const int K = job.nsteps - 1;
+  const int f = job.lg_fan[K];
+  F v;
+  switch (f) {
+    case 8: v = ll_gather_combine<F, 8>(job.ll, job.nin[K], f, job.top_cr, e); break;
+    case 7: v = ll_gather_combine<F, 4>(job.ll, job.nin[K], f, job.top_cr, e); break;
+    case 6: v = ll_gather_combine<F, 2>(job.ll, job.nin[K], f, job.top_cr, e); break;
+    default: v = ll_gather_combine<F, 1>(job.ll, job.nin[K], f, job.top_cr, e); break;
+  }
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) *reinterpret_cast<volatile unsigned*>(job.ll) = e;  // next call: e + 1
+  write_root(job, v);
+}
+
 // Node `idx` of step-k input level has been stored by lane 0 and announced
 // with counter value `old`.  If this warp was the last arrival of its group,
 // evaluate the group's subtree and climb.  Last-arriver combine: who computes
 // a node depends on timing, what is computed never does.
 template <typename F, bool WIDE = false>
-__device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
+__device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old, unsigned ll_e = 0) {
   const int lane = threadIdx.x & 31;
   while (true) {
     const int f = job.lg_fan[k];
@@ -269,6 +378,10 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old) {
     NRMF_TRACE(3, k, 0);
     if (k + 1 == job.nsteps) {
       write_root(job, v);
+      return;
+    }
+    if (WIDE && job.ll != nullptr && k + 2 == job.nsteps) {  // the last step by slots (split kernel)
+      ll_store(job, g, v, ll_e);
       return;
     }
     NRMF_JITTER(1);
@@ -897,6 +1010,8 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   const int64_t grp = blockIdx.x;
   const int k = w / NIT, it = w % NIT;
   NRMF_TRACE(0, 0, 0);
+  const bool ll_comb = job.ll != nullptr && blockIdx.x == 0 && w == 1;
+  const unsigned ll_e = (job.ll != nullptr && (w == 0 || ll_comb)) ? ll_epoch(job) : 0u;
   // are all G tiles of the group full tiles with data?
   bool full = (grp + 1) * G <= job.n_items;
   for (int t = 0; t < G && full; ++t) {
@@ -922,6 +1037,10 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     NRMF_TRACE(5, 0, 0);
   }
   __syncthreads();
+  if (ll_comb) {
+    ll_combine(job, ll_e);
+    return;
+  }
   if (w != 0) return;
   F gv = F(0);
   bool done = false;
@@ -956,13 +1075,17 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     write_root(job, gv);
     return;
   }
-  unsigned old = 0;
   NRMF_JITTER(11);
+  if (job.ll != nullptr && job.nsteps == 1) {  // the group is an input of the last step
+    ll_store(job, grp, gv, ll_e);
+    return;
+  }
+  unsigned old = 0;
   if (lane == 0) {
     job.vals[job.val_off[0] + grp] = gv;
     old = atom_add_release(job.cnt + job.cnt_off[0] + (grp >> job.lg_fan[0]), 1u);
   }
-  climb<F, true>(job, 0, grp, old);
+  climb<F, true>(job, 0, grp, old, ll_e);
   NRMF_TRACE(4, 0, 0);
 }
 
@@ -1098,8 +1221,12 @@ static Plan make_plan(int64_t n_items, int64_t p2, int g0_max, int first_fan = 6
 static size_t tree_ws_bytes(int64_t n_items, int64_t p2, size_t esz) {
   size_t b = 0;
   for (int ff : {6, 4, 8}) {  // fan-in 64 steps, a first CTA step of 16, or a last step up to 256
-    const Plan pl = ff == 8 ? make_plan(n_items, p2, 0, 6, 8) : make_plan(n_items, p2, 0, ff);
-    b = std::max(b, align_up((size_t)pl.n_cnt * 4, 256) + align_up((size_t)pl.n_vals * esz, 256) + 256);
+    for (int g0 = 0; g0 <= (ff == 8 ? 4 : 0); ++g0) {
+      const Plan pl = ff == 8 ? make_plan(n_items, p2, g0, 6, 8) : make_plan(n_items, p2, 0, ff);
+      // the split kernel's last-step slots (ll_*): an epoch word and 16 B per input
+      const size_t ll = ff == 8 && pl.nsteps >= 1 ? align_up(16 * (size_t)(1 + pl.nin[pl.nsteps - 1]), 256) : 0;
+      b = std::max(b, align_up((size_t)pl.n_cnt * 4, 256) + align_up((size_t)pl.n_vals * esz, 256) + ll + 256);
+    }
   }
   return b;
 }
@@ -1125,6 +1252,7 @@ static TreeJob<F> make_job(const F* x, int64_t n_items, int64_t tpc, int64_t ld,
   job.peers = nullptr;
   job.p_err = nullptr;
   job.p_world = job.p_rank = job.p_nr = 0;
+  job.ll = nullptr;
   job.nsteps = pl.nsteps;
   for (int k = 0; k < kMaxSteps; ++k) {
     job.lg_fan[k] = pl.lg_fan[k];
@@ -1189,6 +1317,7 @@ static int g_grid_override = 0;  // test hook: force a grid size (0 = automatic)
 static int g_g0_override = -1;   // dev hook: force the warp-group level count g0 (-1 = automatic)
 static int g_cta_step0 = NRMF_CTA_STEP;  // dev hook: first combine step in shared memory (stream kernel)
 static int g_gap_stream = 1;     // test hook: gapped column blocks on the stream kernel (0: general kernel)
+static int g_split_ll = 1;       // test hook: the split kernel's last step by slots (0: by a counter)
 
 // Launch the tree kernel over items (tiles) with mapping (tpc, ld, len).
 template <typename F>
@@ -1224,12 +1353,19 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
       const Plan pl = combine ? make_plan(n_items, p2, g0s, 6, kMaxFanLg)
                               : make_plan(n_items, int64_t(1) << g0s, g0s);
       const size_t cnt_bytes = align_up((size_t)pl.n_cnt * 4, 256);
-      const size_t need = cnt_bytes + align_up((size_t)pl.n_vals * sizeof(F), 256) + 256;
+      const size_t vals_bytes = align_up((size_t)pl.n_vals * sizeof(F), 256);
+      // the last step by flag-in-data slots (ll_*): no counter, never cleared
+      const bool ll = combine && pl.nsteps >= 1 && g_split_ll;
+      const size_t ll_bytes = ll ? align_up(16 * (size_t)(1 + pl.nin[pl.nsteps - 1]), 256) : 0;
+      const size_t need = cnt_bytes + vals_bytes + ll_bytes + 256;
       if (combine && ws_bytes < need) return NRMF_EWORKSPACE;
-      if (combine && !clean && pl.n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)pl.n_cnt * 4, s) != cudaSuccess)
+      // counters of the steps below the last (none for a one-step plan)
+      const int64_t n_cnt = ll ? pl.cnt_off[pl.nsteps - 1] : pl.n_cnt;
+      if (combine && !clean && n_cnt > 0 && cudaMemsetAsync(ws, 0, (size_t)n_cnt * 4, s) != cudaSuccess)
         return NRMF_ECUDA;
       TreeJob<F> job = make_job(x, n_items, tpc, ld, len, tile_out, out, combine, top_cr, ws, cnt_bytes, pl);
       set_exchange(job, rx);
+      if (ll) job.ll = static_cast<char*>(ws) + cnt_bytes + vals_bytes;
       if (vec) nrmf_split_kernel<F, kVec><<<(unsigned)n_groups, kSplitWarps * 32, 0, s>>>(job);
       else nrmf_split_kernel<F, kScalar><<<(unsigned)n_groups, kSplitWarps * 32, 0, s>>>(job);
       return cudaGetLastError() == cudaSuccess ? NRMF_OK : NRMF_ECUDA;
@@ -1655,6 +1791,11 @@ int nrmf_debug_set_g0(int g0) {
 
 int nrmf_debug_set_gap_stream(int on) {
   g_gap_stream = on != 0;
+  return NRMF_OK;
+}
+
+int nrmf_debug_set_split_ll(int on) {
+  g_split_ll = on != 0;
   return NRMF_OK;
 }
 
