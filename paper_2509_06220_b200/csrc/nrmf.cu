@@ -185,6 +185,27 @@ __device__ __forceinline__ F warp_group_bal_exact(const F* vals, int64_t nvals, 
   return warp_bal_exact6<F>(vals, nvals, base, f, cr);
 }
 
+// The in-register levels over K (a power of two) values a[0..K) with fast
+// checked nodes, each level's K/2^l independent nodes interleaved in ONE
+// v1h_fast_n (separate calls would be issued one chain after the other: ptxas
+// keeps the source order of long FP64 chains).  Root in a[0].
+template <typename F, int K>
+__device__ __forceinline__ void in_lane_levels(F (&a)[K], bool& bad) {
+  if constexpr (K >= 2) {
+    constexpr int H = K / 2;
+    F x[H], y[H], h[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      x[j] = a[2 * j];
+      y[j] = a[2 * j + 1];
+    }
+    v1h_fast_n<true, H>(x, y, h, bad);
+#pragma unroll
+    for (int j = 0; j < H; ++j) a[j] = h[j];
+    in_lane_levels<F, H>(reinterpret_cast<F(&)[H]>(a), bad);
+  }
+}
+
 // Fast-node version: f >= 5: lane l takes the K = 2^(f-5) contiguous values
 // [lK, lK+K) as an in-register tree, then 5 __shfl_xor levels; f < 5: lanes
 // < 2^f one value each, f shuffle levels.  `bad` flags a node outside the
@@ -198,10 +219,7 @@ __device__ __forceinline__ F lane_bal_fast(const F* vals, int64_t nvals, int64_t
     const int64_t i = base + (int64_t)K * lane + j;
     a[j] = i < nvals ? __ldcg(vals + i) : F(0);
   }
-#pragma unroll
-  for (int st = 1; st < K; st <<= 1)
-#pragma unroll
-    for (int j = 0; j < K; j += 2 * st) a[j] = v1h_fast<true>(a[j], a[j + st], bad);
+  in_lane_levels<F, K>(a, bad);
   return a[0];
 }
 
@@ -267,6 +285,7 @@ __device__ __forceinline__ unsigned ll_epoch(const TreeJob<F>& job) {
 }
 template <typename F>
 __device__ __forceinline__ void ll_store(const TreeJob<F>& job, int64_t i, F v, unsigned e) {
+  NRMF_TRACE(9, 0, 0);
   if ((threadIdx.x & 31) == 0) {
     uint32_t lo, hi;
     to_words(v, lo, hi);
@@ -316,10 +335,7 @@ __device__ __noinline__ F ll_gather_combine(const char* ll, int64_t nin, int f, 
     F b[KP];
 #pragma unroll
     for (int j = 0; j < KP; ++j) b[j] = a[j];
-#pragma unroll
-    for (int st = 1; st < KP; st <<= 1)
-#pragma unroll
-      for (int j = 0; j < KP; j += 2 * st) b[j] = v1h_fast<true>(b[j], b[j + st], bad);
+    in_lane_levels<F, KP>(b, bad);
     v = b[0];
     for (int l = 0; l < lv; ++l) v = v1h_fast<true>(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), bad);
     bad = __any_sync(0xffffffffu, lane < (1 << lv) && (bad || v != v));
@@ -338,6 +354,7 @@ template <typename F>
 __device__ void ll_combine(const TreeJob<F>& job, unsigned e) {
   const int K = job.nsteps - 1;
   const int f = job.lg_fan[K];
+  NRMF_TRACE(6, 0, 0);
   F v;
   switch (f) {
     case 8: v = ll_gather_combine<F, 8>(job.ll, job.nin[K], f, job.top_cr, e); break;
@@ -348,6 +365,7 @@ __device__ void ll_combine(const TreeJob<F>& job, unsigned e) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) *reinterpret_cast<volatile unsigned*>(job.ll) = e;  // next call: e + 1
   write_root(job, v);
+  NRMF_TRACE(8, 0, 0);
 }
 
 // Node `idx` of step-k input level has been stored by lane 0 and announced

@@ -2,7 +2,7 @@
 built with -DNRMF_PROBE_TRACE): when warps start, finish groups, climb and
 exit -- where the time between the last group and the kernel's end goes.
 
-    python tools/trace_probe.py variants/trace.so [lg_n]
+    python tools/trace_probe.py build/variants/trace.so [lg_n] [split_ll 0|1]
 """
 import collections
 import ctypes
@@ -21,6 +21,10 @@ def main():
     L.nrmf_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
     L.nrmf_workspace_bytes.restype = ctypes.c_size_t
     L.nrmf_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_uint]
+    if len(sys.argv) > 3:
+        L.nrmf_debug_set_split_ll.argtypes = [ctypes.c_int]
+        L.nrmf_debug_set_split_ll(int(sys.argv[3]))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     n = 1 << lg
     cap = 1 << 20
     buf = torch.zeros(2 * cap, dtype=torch.int64, device="cuda")
@@ -33,6 +37,7 @@ def main():
         s = torch.cuda.current_stream().cuda_stream
         for rep in range(4):
             assert L.nrmf_debug_set_trace(buf.data_ptr(), cap) == 0
+            flush.zero_()                                  # cold L2, as the bench's C1 step
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -48,8 +53,8 @@ def main():
         wid = (a[:, 0] & ((1 << 48) - 1)).astype(np.int64)
         t = (a[:, 1] - a[:, 1].min()).astype(np.int64) / 1e3  # us
         print(f"== {dt} n=2^{lg}: event-timed {ms * 1e3:.1f} us, {len(a)} events")
-        for k, name in ((0, "start"), (5, "batch end"), (1, "group end"), (2, "climb start"), (3, "climb end"),
-                        (4, "exit")):
+        for k, name in ((0, "start"), (5, "batch end"), (1, "group end"), (9, "ll store"), (2, "climb start"),
+                        (3, "climb end"), (6, "ll poll start"), (8, "ll root"), (4, "exit")):
             tk = t[typ == k]
             if len(tk):
                 print(f"  {name:12s} n={len(tk):6d} min {tk.min():8.1f} med {np.median(tk):8.1f} "
