@@ -246,15 +246,15 @@ def time_loop(fn, steps: int, stream, flush=None):
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
     """The oracle (plain C, one host core) on the same workload: each step is a
-    bounded contiguous sample of 2^24 elements of the C3 array (offset varies
-    per step), so the run ends within minutes."""
+    bounded contiguous sample of 2^26 elements of the C3 array (~1 s of CPU;
+    the offset varies per step), so the run ends within a minute or two."""
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
     import oracle
     oracle.build()
     dt = np.float64 if args.config in ("c3", "c1", "c4") else np.float32
-    sample = 1 << 24
+    sample = 1 << 26
     esz = np.dtype(dt).itemsize
     ts = []
     with one_core() as core:
@@ -274,7 +274,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32", "data": "synthetic",
         "config": {"workload": cfg_name(args.config), "n": N_C3, "sample_per_step": sample},
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"2^24 contiguous elements of the {args.config.upper()} array per step",
+                         "sample": f"2^26 contiguous elements of the {args.config.upper()} array per step",
                          "core": core, "nproc": os.cpu_count()},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -633,6 +633,14 @@ def compute_roofline(esz, n, ms, f_ghz, hbm_peak):
         t_comp = t_issue
     d["frac"] = round(t_comp / t, 4)
     d["t_compute_ms"] = round(t_comp * 1e3, 4)
+    if c.get("rf_read_cycles_per_warp_node"):
+        # a model, not a hardware peak: register-file read cycles per warp
+        # instruction from the bank model of DESIGN.md §8, summed over the
+        # executed instructions (ncu source page) -- it predicts the kernel's
+        # time (the instructions do not overlap each other's operand reads)
+        t_rf = warp_nodes * c["rf_read_cycles_per_warp_node"] / slots
+        d["rf_model"] = {"read_cycles_per_warp_node": c["rf_read_cycles_per_warp_node"],
+                         "t_ms": round(t_rf * 1e3, 4), "ratio_to_kernel": round(t_rf / t, 4)}
     d["binding"] = "hbm" if t_hbm >= t_comp else "alu"
     d["binding_frac"] = round(max(t_hbm, t_comp) / t, 4)
     return d
