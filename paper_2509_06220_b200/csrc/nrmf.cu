@@ -554,9 +554,6 @@ struct WarpSmem {
   static constexpr uint32_t kBars = kXs + kGroupXsBytes<F>;
   static constexpr uint32_t kBytes = (kBars + kStages * 8 + 127) / 128 * 128;
 };
-static_assert(WarpSmem<double>::kBars % 16 == 0 && WarpSmem<float>::kBars % 16 == 0 &&
-                  WarpSmem<double>::kBytes % 16 == 0 && WarpSmem<float>::kBytes % 16 == 0,
-              "StreamLoader toggles between the two mbarriers by flipping address bit 3");
 static_assert(kWarps * WarpSmem<double>::kBytes + CtaSmem<double>::kBytes <= 227 * 1024 &&
                   kWarps * WarpSmem<float>::kBytes + CtaSmem<float>::kBytes <= 227 * 1024,
               "stream kernel shared memory");
@@ -582,11 +579,6 @@ struct StreamLoader {
 
   uint32_t my_s;         // this warp's block (WarpSmem)
   uint32_t consumed;     // stages consumed (warp-uniform)
-  // the current stage, kept incrementally (two stages: two XORs and a phase
-  // flip per batch instead of recomputing slot, offsets and parity from
-  // `consumed`): its byte offset in the ring, its mbarrier, the wait parity,
-  // and this lane's row-0 address in the ring
-  uint32_t stage_off, bar_cur, par, ring_lane;
   const char* p_ptr;     // next batch to load
   int p_left;            // batches left in its group
   int groups_left;       // further groups after it (-1: nothing left to load)
@@ -609,19 +601,11 @@ struct StreamLoader {
     col_left = (int)(tpc - tt) * (Cfg<F>::J / kBatch);
   }
 
-  __device__ __forceinline__ void start() {  // after my_s is set; consumed = 0
-    stage_off = 0;
-    bar_cur = my_s + L::kBars;
-    par = 0;
-    ring_lane = my_s + L::kRing + (threadIdx.x & 31) * 16;
-  }
   __device__ __forceinline__ void issue(uint32_t slot) {
-    issue_at(slot * kBatchBytes, my_s + L::kBars + slot * 8);
-  }
-  __device__ __forceinline__ void issue_at(uint32_t off, uint32_t bar) {
     if (groups_left < 0) return;
     if ((threadIdx.x & 31) == 0)
-      bulk_load(my_s + L::kRing + off, p_ptr, kBatchBytes, bar, policy_evict_first());
+      bulk_load(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
+                policy_evict_first());
     p_ptr += kBatchBytes;
     if (GAP && --col_left == 0) {
       col_left = col_batches;
@@ -639,8 +623,7 @@ struct StreamLoader {
     }
   }
   __device__ __forceinline__ void begin(int) {
-    if constexpr (kStages == 2) mbar_wait(bar_cur, par);
-    else mbar_wait(my_s + L::kBars + (consumed % kStages) * 8, (consumed / kStages) & 1);
+    mbar_wait(my_s + L::kBars + (consumed % kStages) * 8, (consumed / kStages) & 1);
   }
   // consume `nb` batches without reading them (the ring keeps streaming)
   __device__ __noinline__ void drain(int nb) {
@@ -655,9 +638,8 @@ struct StreamLoader {
     for (int v = 0; v < Cfg<F>::V; ++v) o[v] = F(1) + F(row * 7 + v) * F(1e-3) + F(consumed & 3);
     return;
 #endif
-    const uint32_t addr = kStages == 2 ? ring_lane + stage_off + row * (kBatchBytes / kBatch)
-                                       : my_s + L::kRing + (consumed % kStages) * kBatchBytes +
-                                             (threadIdx.x & 31) * 16 + row * (kBatchBytes / kBatch);
+    const uint32_t addr = my_s + L::kRing + (consumed % kStages) * kBatchBytes + (threadIdx.x & 31) * 16 +
+                          row * (kBatchBytes / kBatch);
     if constexpr (sizeof(F) == 8) {
       double a0, a1;
       asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0), "=d"(a1) : "r"(addr) : "memory");
@@ -675,14 +657,6 @@ struct StreamLoader {
   }
   __device__ __forceinline__ void end(int) {
     __syncwarp();  // every lane holds its leaves: the stage may be refilled
-    if constexpr (kStages == 2) {
-      issue_at(stage_off, bar_cur);  // refill the stage just consumed
-      stage_off ^= kBatchBytes;
-      bar_cur ^= 8u;                 // the two barriers are 16-byte aligned: a bit flip
-      par ^= stage_off == 0 ? 1u : 0u;
-      ++consumed;
-      return;
-    }
     const uint32_t slot = consumed % kStages;
     ++consumed;
     issue(slot);
@@ -853,7 +827,6 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     }
     __syncwarp();
     sl.consumed = 0;
-    sl.start();
     sl.group_batches = G * (Cfg<F>::J / kBatch);
     sl.p_left = sl.group_batches;
     // groups gw, gw + W, ... below n_full: this warp streams 1 + groups_left of them
