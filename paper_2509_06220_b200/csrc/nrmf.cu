@@ -39,6 +39,9 @@ constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's l
 #ifndef NRMF_USE_TMA
 #define NRMF_USE_TMA 1        // 0: aligned full tiles use direct LDG.128 instead of the TMA ring
 #endif
+#ifndef NRMF_ELECT_ISSUE
+#define NRMF_ELECT_ISSUE 0    // 1: stream loader issues the TMA copy with elect.sync inside the asm (A/B pending)
+#endif
 #ifndef NRMF_SKIP_FLAGGED
 #define NRMF_SKIP_FLAGGED 0   // 1: stream kernel stops evaluating a group at its first flagged tile (C5 -6 %, DNRMF +1.3 %: off)
 #endif
@@ -264,38 +267,54 @@ __device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
 }
 
 // ---------------------------------------------------------------------------
-// Last combine step of the split kernel without a counter (small calls: the
-// latency of the release fence, the atomic round trip and the re-read of the
-// values was ~2 us of a 14 us call).  Each input of the last step is written
-// by the warp that produced it into its 16-byte slot together with the call's
-// epoch e, twice -- {lo32, e, hi32, e}, each 8-byte half one store/load unit
-// (the flag-in-data scheme of the peer exchange, nrmf_p2p.cuh) -- and ONE
-// warp (CTA 0, warp 1: it has no group work of its own after its batch)
-// polls the slots until every one carries e, then evaluates the step's
-// balanced subtree in registers (the same tree as warp_group_bal) and writes
-// the root.  The epoch is a word in the workspace: every producer reads it at
-// its start (e = word + 1) and the combiner advances it after the last slot
-// arrived, so nothing is cleared between calls and graph replays work; a
-// workspace of garbage gives a random e that a garbage slot matches in both
-// halves with probability 2^-64.  Only one warp waits, on producers that never
-// wait themselves, so the grid needs no co-residency.
+// Last combine step of the split kernel without a counter (small calls: no
+// counter to clear, no release fence, no atomic round trip).  Each input of
+// the last step is written by the warp that produced it into its 16-byte slot
+// together with the call's 64-bit tag (t1, t2) -- {lo32, t1, hi32, t2}, each
+// 8-byte half one store/load unit (the flag-in-data scheme of the peer
+// exchange, nrmf_p2p.cuh) -- and ONE warp (CTA 0, warp 1: it has no group work
+// of its own after its batch) polls the slots until every one carries the
+// tag, evaluates the step's balanced subtree in registers (the same tree as
+// warp_group_bal), clears the slots it read and writes the root.
+// The tag must never be found in stale memory: the workspace header holds a
+// 64-bit count of completed calls c (read by every producer at its start,
+// advanced by the combiner after the last slot arrived, so graph replays
+// work), and the tag is a 64-bit hash of (c + 1, the header's address), both
+// halves odd.  A slot is only ever matched by the tag it was written with:
+// stale slots of this layout were cleared by the call that read them (even if
+// the header was later reset by another call reusing the workspace, its tag
+// sequence restarts on cleared slots), slots written by another layout carry
+// tags of another address, and garbage matches with probability 2^-64.  Only
+// one warp waits, on producers that never wait themselves, so the grid needs
+// no co-residency.
+__device__ __forceinline__ uint64_t ll_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// this call's number c + 1 (the combiner stores it back) and its tag
 template <typename F>
-__device__ __forceinline__ unsigned ll_epoch(const TreeJob<F>& job) {
-  return *reinterpret_cast<volatile unsigned*>(job.ll) + 1u;
+__device__ __forceinline__ uint64_t ll_call(const TreeJob<F>& job) {
+  return *reinterpret_cast<volatile unsigned long long*>(job.ll) + 1ull;
+}
+__device__ __forceinline__ uint64_t ll_tag(const char* ll, uint64_t call) {
+  return ll_mix(call ^ ll_mix(reinterpret_cast<uintptr_t>(ll))) | 0x0000000100000001ull;
 }
 template <typename F>
-__device__ __forceinline__ void ll_store(const TreeJob<F>& job, int64_t i, F v, unsigned e) {
+__device__ __forceinline__ void ll_store(const TreeJob<F>& job, int64_t i, F v, uint64_t tag) {
   NRMF_TRACE(9, 0, 0);
   if ((threadIdx.x & 31) == 0) {
     uint32_t lo, hi;
     to_words(v, lo, hi);
-    st_ll(job.ll + 16 * (i + 1), lo, hi, e);
+    st_ll2(job.ll + 16 * (i + 1), lo, hi, (uint32_t)tag, (uint32_t)(tag >> 32));
   }
 }
 // KP inputs per lane (lanes < 2^f when f <= 5): poll, then the fast tree with
 // the exact fallback (as warp_group_bal: any flagged node or NaN).
 template <typename F, int KP>
-__device__ __noinline__ F ll_gather_combine(const char* ll, int64_t nin, int f, int cr, unsigned e) {
+__device__ __noinline__ F ll_gather_combine(char* ll, int64_t nin, int f, int cr, uint64_t tag) {
+  const uint32_t t1 = (uint32_t)tag, t2 = (uint32_t)(tag >> 32);
   const int lane = threadIdx.x & 31;
   F a[KP];
   bool ready[KP];
@@ -312,7 +331,7 @@ __device__ __noinline__ F ll_gather_combine(const char* ll, int64_t nin, int f, 
       if (ready[j]) continue;
       uint32_t lo, e0, hi, e1;
       ld_ll(ll + 16 * ((int64_t)lane * KP + j + 1), lo, e0, hi, e1);
-      if (e0 == e && e1 == e) {
+      if (e0 == t1 && e1 == t2) {
         a[j] = from_words<F>(lo, hi);
         ready[j] = true;
       } else {
@@ -327,6 +346,14 @@ __device__ __noinline__ F ll_gather_combine(const char* ll, int64_t nin, int f, 
       break;
     }
     if (spins > 32) __nanosleep(32);
+  }
+  // clear the slots read: a later call with this layout whose call number
+  // repeats (header reset by another call sharing the workspace) finds no
+  // stale match
+#pragma unroll
+  for (int j = 0; j < KP; ++j) {
+    const int64_t i = (int64_t)lane * KP + j;
+    if (i < nin && (KP > 1 || lane < (1 << f))) st_ll2(ll + 16 * (i + 1), 0u, 0u, 0u, 0u);
   }
   const int lv = f < 5 ? f : 5;
   bool bad = cr != 0;
@@ -351,19 +378,20 @@ __device__ __noinline__ F ll_gather_combine(const char* ll, int64_t nin, int f, 
   return v;
 }
 template <typename F>
-__device__ void ll_combine(const TreeJob<F>& job, unsigned e) {
+__device__ void ll_combine(const TreeJob<F>& job, uint64_t call) {
   const int K = job.nsteps - 1;
   const int f = job.lg_fan[K];
+  const uint64_t tag = ll_tag(job.ll, call);
   NRMF_TRACE(6, 0, 0);
   F v;
   switch (f) {
-    case 8: v = ll_gather_combine<F, 8>(job.ll, job.nin[K], f, job.top_cr, e); break;
-    case 7: v = ll_gather_combine<F, 4>(job.ll, job.nin[K], f, job.top_cr, e); break;
-    case 6: v = ll_gather_combine<F, 2>(job.ll, job.nin[K], f, job.top_cr, e); break;
-    default: v = ll_gather_combine<F, 1>(job.ll, job.nin[K], f, job.top_cr, e); break;
+    case 8: v = ll_gather_combine<F, 8>(job.ll, job.nin[K], f, job.top_cr, tag); break;
+    case 7: v = ll_gather_combine<F, 4>(job.ll, job.nin[K], f, job.top_cr, tag); break;
+    case 6: v = ll_gather_combine<F, 2>(job.ll, job.nin[K], f, job.top_cr, tag); break;
+    default: v = ll_gather_combine<F, 1>(job.ll, job.nin[K], f, job.top_cr, tag); break;
   }
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) *reinterpret_cast<volatile unsigned*>(job.ll) = e;  // next call: e + 1
+  if ((threadIdx.x & 31) == 0) *reinterpret_cast<volatile unsigned long long*>(job.ll) = call;  // completed calls
   write_root(job, v);
   NRMF_TRACE(8, 0, 0);
 }
@@ -373,7 +401,7 @@ __device__ void ll_combine(const TreeJob<F>& job, unsigned e) {
 // evaluate the group's subtree and climb.  Last-arriver combine: who computes
 // a node depends on timing, what is computed never does.
 template <typename F, bool WIDE = false>
-__device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old, unsigned ll_e = 0) {
+__device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old, uint64_t ll_t = 0) {
   const int lane = threadIdx.x & 31;
   while (true) {
     const int f = job.lg_fan[k];
@@ -399,7 +427,7 @@ __device__ void climb(const TreeJob<F>& job, int k, int64_t idx, unsigned old, u
       return;
     }
     if (WIDE && job.ll != nullptr && k + 2 == job.nsteps) {  // the last step by slots (split kernel)
-      ll_store(job, g, v, ll_e);
+      ll_store(job, g, v, ll_t);
       return;
     }
     NRMF_JITTER(1);
@@ -603,9 +631,14 @@ struct StreamLoader {
 
   __device__ __forceinline__ void issue(uint32_t slot) {
     if (groups_left < 0) return;
+#if NRMF_ELECT_ISSUE
+    bulk_load_warp(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
+                   policy_evict_first());
+#else
     if ((threadIdx.x & 31) == 0)
       bulk_load(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
                 policy_evict_first());
+#endif
     p_ptr += kBatchBytes;
     if (GAP && --col_left == 0) {
       col_left = col_batches;
@@ -1029,7 +1062,9 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   const int k = w / NIT, it = w % NIT;
   NRMF_TRACE(0, 0, 0);
   const bool ll_comb = job.ll != nullptr && blockIdx.x == 0 && w == 1;
-  const unsigned ll_e = (job.ll != nullptr && (w == 0 || ll_comb)) ? ll_epoch(job) : 0u;
+  // this call's number (the combiner) and slot tag (the producers: warp 0s)
+  const uint64_t ll_c = (job.ll != nullptr && (w == 0 || ll_comb)) ? ll_call(job) : 0ull;
+  const uint64_t ll_t = job.ll != nullptr && w == 0 ? ll_tag(job.ll, ll_c) : 0ull;
   // are all G tiles of the group full tiles with data?
   bool full = (grp + 1) * G <= job.n_items;
   for (int t = 0; t < G && full; ++t) {
@@ -1056,7 +1091,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   }
   __syncthreads();
   if (ll_comb) {
-    ll_combine(job, ll_e);
+    ll_combine(job, ll_c);
     return;
   }
   if (w != 0) return;
@@ -1095,7 +1130,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   }
   NRMF_JITTER(11);
   if (job.ll != nullptr && job.nsteps == 1) {  // the group is an input of the last step
-    ll_store(job, grp, gv, ll_e);
+    ll_store(job, grp, gv, ll_t);
     return;
   }
   unsigned old = 0;
@@ -1103,7 +1138,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     job.vals[job.val_off[0] + grp] = gv;
     old = atom_add_release(job.cnt + job.cnt_off[0] + (grp >> job.lg_fan[0]), 1u);
   }
-  climb<F, true>(job, 0, grp, old, ll_e);
+  climb<F, true>(job, 0, grp, old, ll_t);
   NRMF_TRACE(4, 0, 0);
 }
 

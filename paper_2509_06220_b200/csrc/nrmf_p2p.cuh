@@ -46,6 +46,10 @@ __device__ __forceinline__ void st_ll(char* p, uint32_t lo, uint32_t hi, uint32_
   asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(lo), "r"(e), "r"(hi), "r"(e)
                : "memory");
 }
+__device__ __forceinline__ void st_ll2(char* p, uint32_t lo, uint32_t hi, uint32_t e0, uint32_t e1) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(lo), "r"(e0), "r"(hi), "r"(e1)
+               : "memory");
+}
 __device__ __forceinline__ void ld_ll(const char* p, uint32_t& lo, uint32_t& e0, uint32_t& hi, uint32_t& e1) {
   asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(lo), "=r"(e0), "=r"(hi), "=r"(e1)
                : "l"(p) : "memory");

@@ -87,3 +87,34 @@ def test_ll_graph_replay(nrmf):
         g.replay()
     torch.cuda.synchronize()
     assert bits(out.cpu().numpy(), np.float64) == bits(oracle.nrmf(x1), np.float64)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_ll_one_workspace_shared_by_many_shapes(nrmf, seed):
+    """One workspace shared by calls of many sizes and both precisions in a
+    random order (the Python binding caches one workspace per stream and kind,
+    so a test suite does exactly this): the layouts overlap -- one shape's
+    slots and counters sit on another's header -- and no call may pick up a
+    stale slot.  300 calls, each checked against the oracle."""
+    import ctypes
+    L = nrmf.lib()
+    rng = np.random.default_rng(seed)
+    shapes = [(n, dt) for n in (3 * T + 5, 33 * T, 64 * T + 1, 100 * T + 3, 256 * T, 300 * T + 7, 591 * T, 1000 * T)
+              for dt in (np.float64, np.float32)]
+    data = {}
+    for n, dt in shapes:
+        x = gen.normal(n + (dt == np.float32), n, dtype=dt)
+        data[(n, dt)] = (torch.from_numpy(x).cuda(), bits(oracle.nrmf(x), dt))
+    nb = max(L.nrmf_workspace_bytes(n, 8) for n, _ in shapes)
+    ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    outs = {k: torch.empty((), dtype=v[0].dtype, device="cuda") for k, v in data.items()}
+    for i in range(300):
+        k = shapes[int(rng.integers(len(shapes)))]
+        xd, want = data[k]
+        f = L.nrmf_d if k[1] == np.float64 else L.nrmf_s
+        assert f(k[0], xd.data_ptr(), outs[k].data_ptr(), ws.data_ptr(), nb, s) == 0
+        torch.cuda.synchronize()
+        assert bits(outs[k].cpu().numpy(), k[1]) == want, (i, k)
+        if i % 50 == 49:
+            ws[: 4096].zero_()      # another user of the memory resets a prefix (headers of small layouts)
