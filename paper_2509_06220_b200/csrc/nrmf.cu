@@ -39,9 +39,6 @@ constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's l
 #ifndef NRMF_USE_TMA
 #define NRMF_USE_TMA 1        // 0: aligned full tiles use direct LDG.128 instead of the TMA ring
 #endif
-#ifndef NRMF_ELECT_ISSUE
-#define NRMF_ELECT_ISSUE 0    // 1: stream loader issues the TMA copy with elect.sync inside the asm (A/B pending)
-#endif
 #ifndef NRMF_SKIP_FLAGGED
 #define NRMF_SKIP_FLAGGED 0   // 1: stream kernel stops evaluating a group at its first flagged tile (C5 -6 %, DNRMF +1.3 %: off)
 #endif
@@ -631,14 +628,9 @@ struct StreamLoader {
 
   __device__ __forceinline__ void issue(uint32_t slot) {
     if (groups_left < 0) return;
-#if NRMF_ELECT_ISSUE
-    bulk_load_warp(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
-                   policy_evict_first());
-#else
     if ((threadIdx.x & 31) == 0)
       bulk_load(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
                 policy_evict_first());
-#endif
     p_ptr += kBatchBytes;
     if (GAP && --col_left == 0) {
       col_left = col_batches;
