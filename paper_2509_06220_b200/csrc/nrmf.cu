@@ -630,7 +630,7 @@ struct StreamLoader {
     if (groups_left < 0) return;
     if ((threadIdx.x & 31) == 0)
       bulk_load(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
-                policy_evict_first());
+                stream_l2_policy());
     p_ptr += kBatchBytes;
     if (GAP && --col_left == 0) {
       col_left = col_batches;
@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     pl.W = W;
     pl.G = G;
     pl.n_groups = n_groups;
-    pl.policy = policy_evict_first();
+    pl.policy = stream_l2_policy();
     pl.x = job.x;
     pl.n_items = job.n_items;
     pl.tpc = job.tpc;
