@@ -19,12 +19,17 @@ bad = 0
 for i in range(N):
     n = int(np.exp(rng.uniform(0, np.log(1 << 24))))
     dt = np.float64 if rng.integers(2) else np.float32
-    dist = ["normal", "uniform", "sme"][rng.integers(3)]
+    dist = ["normal", "uniform", "sme", "extreme"][rng.integers(4)]
+    if dist == "extreme" and dt != np.float64:
+        dist = "sme"
     off = int(rng.integers(0, 4))           # elements of offset: 0 keeps 16-byte alignment only sometimes
     top = "cr" if rng.integers(8) == 0 else "v1"
     seed = int(rng.integers(1, 1 << 30))
     m = n + off
-    x = {"normal": gen.normal, "uniform": gen.uniform_pm1, "sme": gen.sme}[dist](seed, m, dtype=dt)
+    if dist == "extreme":
+        x = gen.extreme(seed, m, ["lit", "fin", "fin2"][seed % 3])
+    else:
+        x = {"normal": gen.normal, "uniform": gen.uniform_pm1, "sme": gen.sme}[dist](seed, m, dtype=dt)
     xd = torch.from_numpy(x).cuda()[off:]
     grid = g0 = -1
     cta = True
@@ -32,6 +37,7 @@ for i in range(N):
         grid = int(rng.choice([0, 1, 2, 3, 7, 16, 37, 148, 296]))
         g0 = int(rng.integers(-1, 5))
         cta = bool(rng.integers(4))
+        nrmf._debug_set_split_ll(bool(rng.integers(4)))
         nrmf._debug_set_grid(grid)
         nrmf._debug_set_g0(g0)
         nrmf._debug_set_cta_step(cta)
@@ -40,6 +46,7 @@ for i in range(N):
         nrmf._debug_set_grid(0)
         nrmf._debug_set_g0(-1)
         nrmf._debug_set_cta_step(True)
+        nrmf._debug_set_split_ll(True)
     e = oracle.nrmf(x[off:], top=top)
     ok = np.asarray(r, dtype=dt).tobytes() == np.asarray(e, dtype=dt).tobytes()
     if not ok:
