@@ -39,6 +39,9 @@ constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's l
 #ifndef NRMF_USE_TMA
 #define NRMF_USE_TMA 1        // 0: aligned full tiles use direct LDG.128 instead of the TMA ring
 #endif
+#ifndef NRMF_SHORT_PAIRS
+#define NRMF_SHORT_PAIRS 1    // columns of rows <= 2 batches: two per warp at a time
+#endif
 #ifndef NRMF_SKIP_FLAGGED
 #define NRMF_SKIP_FLAGGED 0   // 1: stream kernel stops evaluating a group at its first flagged tile (C5 -6 %, DNRMF +1.3 %: off)
 #endif
@@ -823,6 +826,28 @@ __device__ __forceinline__ F single_tile(const TreeJob<F>& job, int64_t tau) {
   return warp_tile_exact<F, kPred>(tb, (int)remv);
 }
 
+// Values of tiles tau and tau + 1 (short columns: partial tiles of one
+// length), beyond the data +0; bad or NaN: each tile by the exact path.
+template <typename F>
+__device__ __forceinline__ void short_pair(const TreeJob<F>& job, int64_t tau, F (&tv)[2]) {
+  tv[0] = tv[1] = F(0);
+  if (tau >= job.n_items) return;
+  const F *tb0, *tb1;
+  int64_t remv;
+  tile_at(job, tau, tb0, remv);
+  if (tau + 1 >= job.n_items) {
+    tv[0] = single_tile<F, false>(job, tau);
+    return;
+  }
+  tile_at(job, tau + 1, tb1, remv);
+  bool bad = false;
+  warp_tiles_short2<F>(tb0, tb1, (int)remv, bad, tv[0], tv[1]);
+  if (bad || tv[0] != tv[0] || tv[1] != tv[1]) {
+    tv[0] = warp_tile_exact<F, kPred>(tb0, (int)remv);
+    tv[1] = warp_tile_exact<F, kPred>(tb1, (int)remv);
+  }
+}
+
 template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false>
 __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(const TreeJob<F> job) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -964,6 +989,25 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         gv[0] = v;
         group_done = true;
       }
+    }
+    // short columns (every tile one column of rows <= 2 batches): two
+    // columns at a time (warp_tiles_short2), merged like the loop below
+    if (!kStream && NRMF_SHORT_PAIRS && !group_done && job.tpc == 1 && job.ld != 0 && G >= 2 &&
+        job.len <= 2 * kBatch * Cfg<F>::LANES) {
+      for (int k = 0; k < G; k += 2) {  // rolled
+        F tv[2];
+        short_pair<F>(job, grp * G + k, tv);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int64_t tau = grp * G + k + t;
+          if (job.tile_out != nullptr && lane == 0 && tau < job.n_items) job.tile_out[tau] = tv[t];
+          gv[0] = tv[t];
+          if (G == 8) counter_merge<F, 1, 8>(k + t, gv, s0, s1, s2, ne);
+          else if (G == 4) counter_merge<F, 1, 4>(k + t, gv, s0, s1, s2, ne);
+          else counter_merge<F, 1, 2>(k + t, gv, s0, s1, s2, ne);
+        }
+      }
+      group_done = true;
     }
     // the stream kernel merges a (partial) group's tile values through its xs
     // area (groups of up to 16 tiles); the other kernels by counter_merge

@@ -1,0 +1,73 @@
+"""Short columns (rows <= 2 batches of rows: 1024 fp64 / 2048 fp32) evaluated
+two per warp (warp_tiles_short2): the same tree as one column at a time, so
+the oracle's bits for every column norm and the Frobenius norm -- on the
+persistent kernel (many columns), with forced small grids, odd column counts
+(a last unpaired column), zero / NaN / inf / huge / subnormal columns (the
+exact fallback of a pair), leading dimensions > rows, both tops."""
+import numpy as np
+import pytest
+import torch
+
+import nrmf_inputs as gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nrmf():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2509_06220_b200 import _build
+    _build.build()
+    import paper_2509_06220_b200 as m
+    m.lib()
+    torch.cuda.set_device(0)
+    return m
+
+
+def run(nrmf, r, c, ld, dt, top="v1", specials=False, seed=1):
+    A = gen.colscaled_normal(seed, r, c, ld=ld, dtype=dt)
+    if specials:
+        rng = np.random.default_rng(seed)
+        cols = rng.choice(c, 12, replace=False)
+        A[cols[0] * ld: cols[0] * ld + r] = 0
+        A[cols[1] * ld + r // 2] = np.nan
+        A[cols[2] * ld] = np.inf
+        A[cols[3] * ld: cols[3] * ld + r] = np.finfo(dt).max / 4
+        A[cols[4] * ld: cols[4] * ld + r] = np.finfo(dt).tiny / 8
+        A[cols[5] * ld + r - 1] = -np.finfo(dt).max
+    T = torch.from_numpy(A).cuda().as_strided((r, c), (1, ld))
+    col, fr = nrmf.cols(T, top=top)
+    ecol, efr = oracle.cols(A, r, c, ld, top=top)
+    got, want = col.cpu().numpy(), ecol
+    same = (got.tobytes() == want.tobytes()) or np.array_equal(got, want, equal_nan=True)
+    assert same, (r, c, ld, np.nonzero(~((got == want) | (np.isnan(got) & np.isnan(want))))[0][:5])
+    f = fr.cpu().numpy()
+    assert f.tobytes() == np.asarray(efr, dtype=dt).tobytes() or (np.isnan(f) and np.isnan(efr))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("r", [1, 5, 64, 127, 500, 1000, 1024, 2048])
+def test_short_columns_parity(nrmf, dt, r):
+    if dt == np.float64 and r > 1024:
+        r = 1023
+    for c, ld in ((5001, r), (7777, r + 3)):
+        run(nrmf, r, c, ld, dt)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_short_columns_specials_and_tops(nrmf, dt):
+    for r in (7, 300, 1000):
+        run(nrmf, r, 6001, r, dt, specials=True, seed=r)
+        run(nrmf, r, 6001, r + 1, dt, top="cr", seed=r + 1)
+
+
+@pytest.mark.parametrize("grid", [1, 3, 7])
+def test_short_columns_forced_grids(nrmf, grid):
+    nrmf._debug_set_grid(grid)
+    try:
+        for dt in (np.float64, np.float32):
+            run(nrmf, 333, 999, 333, dt, seed=grid)
+            run(nrmf, 1000, 64, 1001, dt, specials=True, seed=grid + 10)
+    finally:
+        nrmf._debug_set_grid(0)
