@@ -403,6 +403,23 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if dist and p2p:
+        # the fused peer exchange has only ever run on a 1-rank group: check it
+        # on this box before timing it -- no rank timed out and every rank holds
+        # the same bits -- and otherwise time the NCCL exchange and say so
+        hx = torch.tensor([np.asarray(out.cpu().item(), dtype=dt).view(np.int64 if esz == 8 else np.int32).item(),
+                           int(pgroup.err.item())], dtype=torch.int64, device=device)
+        allh = torch.zeros(2 * world, dtype=torch.int64, device=device)
+        td.all_gather_into_tensor(allh, hx)
+        vals = allh.view(world, 2).tolist()
+        if any(e != 0 for _, e in vals) or len({v for v, _ in vals}) != 1:
+            p2p, p2p_note = False, f"P2P exchange check failed on this box ({vals}); NCCL exchange"
+            call = lambda: nrmf.dist(x, n, comm=comm, out=out)  # noqa: E731
+            launches_per_step = 2
+            graph = nrmf.capture(call) if use_graph else None
+            for _ in range(args.warmup):
+                step()
+            torch.cuda.synchronize()
     if dist:
         td.barrier()
     # inputs below 4x the 126 MB L2 (C1: 8 MiB): flush L2 before every timed step
