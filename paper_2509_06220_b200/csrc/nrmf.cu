@@ -992,7 +992,9 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     }
     // short columns (every tile one column of rows <= 2 batches): two
     // columns at a time (warp_tiles_short2), merged like the loop below
-    if (!kStream && NRMF_SHORT_PAIRS && !group_done && job.tpc == 1 && job.ld != 0 && G >= 2 &&
+    // (16-byte aligned column blocks only: in the element-load kernel, which
+    // also serves unaligned vectors, the extra path cost those 8 %)
+    if (TMA && !kStream && NRMF_SHORT_PAIRS && !group_done && job.tpc == 1 && job.ld != 0 && G >= 2 &&
         job.len <= 2 * kBatch * Cfg<F>::LANES) {
       for (int k = 0; k < G; k += 2) {  // rolled
         F tv[2];

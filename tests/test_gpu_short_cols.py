@@ -1,5 +1,6 @@
-"""Short columns (rows <= 2 batches of rows: 1024 fp64 / 2048 fp32) evaluated
-two per warp (warp_tiles_short2): the same tree as one column at a time, so
+"""Short columns (rows <= 2 batches of rows: 1024 fp64 / 2048 fp32, 16-byte
+aligned columns) evaluated two per warp (warp_tiles_short2): the same tree as
+one column at a time, so
 the oracle's bits for every column norm and the Frobenius norm -- on the
 persistent kernel (many columns), with forced small grids, odd column counts
 (a last unpaired column), zero / NaN / inf / huge / subnormal columns (the
@@ -51,15 +52,19 @@ def run(nrmf, r, c, ld, dt, top="v1", specials=False, seed=1):
 def test_short_columns_parity(nrmf, dt, r):
     if dt == np.float64 and r > 1024:
         r = 1023
-    for c, ld in ((5001, r), (7777, r + 3)):
+    a = 2 if dt == np.float64 else 4           # 16-byte aligned columns: the paired path
+    lda = -(-r // a) * a
+    for c, ld in ((5001, lda), (7777, lda + a), (4099, r + 3)):   # the last: element loads, one at a time
         run(nrmf, r, c, ld, dt)
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_short_columns_specials_and_tops(nrmf, dt):
+    a = 2 if dt == np.float64 else 4
     for r in (7, 300, 1000):
-        run(nrmf, r, 6001, r, dt, specials=True, seed=r)
-        run(nrmf, r, 6001, r + 1, dt, top="cr", seed=r + 1)
+        lda = -(-r // a) * a
+        run(nrmf, r, 6001, lda, dt, specials=True, seed=r)
+        run(nrmf, r, 6001, lda + a, dt, top="cr", seed=r + 1)
 
 
 @pytest.mark.parametrize("grid", [1, 3, 7])
@@ -67,7 +72,8 @@ def test_short_columns_forced_grids(nrmf, grid):
     nrmf._debug_set_grid(grid)
     try:
         for dt in (np.float64, np.float32):
-            run(nrmf, 333, 999, 333, dt, seed=grid)
-            run(nrmf, 1000, 64, 1001, dt, specials=True, seed=grid + 10)
+            run(nrmf, 333, 999, 336, dt, seed=grid)
+            run(nrmf, 1000, 64, 1000, dt, specials=True, seed=grid + 10)
+            run(nrmf, 333, 99, 333, dt, seed=grid + 20)
     finally:
         nrmf._debug_set_grid(0)

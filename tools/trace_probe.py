@@ -2,7 +2,7 @@
 built with -DNRMF_PROBE_TRACE): when warps start, finish groups, climb and
 exit -- where the time between the last group and the kernel's end goes.
 
-    python tools/trace_probe.py build/variants/trace.so [lg_n] [split_ll 0|1]
+    python tools/trace_probe.py build/variants/trace.so [lg_n] [split_ll 0|1] [pad KiB before ws]
 """
 import collections
 import ctypes
@@ -31,8 +31,11 @@ def main():
     for dt in (torch.float32, torch.float64):
         x = torch.randn(n, dtype=dt, device="cuda")
         esz = x.element_size()
+        pad = torch.zeros(max(1, int(sys.argv[4]) if len(sys.argv) > 4 else 0) * 1024, dtype=torch.uint8,
+                          device="cuda")
         ws = torch.zeros(L.nrmf_workspace_bytes(n, esz), dtype=torch.uint8, device="cuda")
         out = torch.empty((), dtype=dt, device="cuda")
+        print(f"ws at {ws.data_ptr():#x}, out at {out.data_ptr():#x}", flush=True)
         f = L.nrmf_d if esz == 8 else L.nrmf_s
         s = torch.cuda.current_stream().cuda_stream
         for rep in range(4):
