@@ -590,6 +590,13 @@ def _debug_set_gap_stream(on: bool):
     L.nrmf_debug_set_gap_stream(1 if on else 0)
 
 
+def _debug_set_unal_stream(on: bool):
+    """Test hook: unaligned vectors on the stream kernel (default on) or the element-load kernel."""
+    L = _load()
+    L.nrmf_debug_set_unal_stream.argtypes = [ctypes.c_int]
+    L.nrmf_debug_set_unal_stream(1 if on else 0)
+
+
 def _debug_set_split_ll(on: bool):
     """Test hook: the split kernel's last combine step by flag-in-data slots (default on) or a counter."""
     L = _load()

@@ -30,6 +30,9 @@ namespace nrmf {
 // ------------------------------------------------------------------ kernels
 constexpr int kMaxSteps = 8;
 constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's last one up to 8 (fan-in 256)
+#ifndef NRMF_SAFE_MODE
+#define NRMF_SAFE_MODE 0      // stream kernel: safe-node groups from the ring after a flagged group
+#endif
 #ifndef NRMF_STAGES
 #define NRMF_STAGES 2         // TMA ring depth per warp (batches of 4 KiB)
 #endif
@@ -574,16 +577,19 @@ struct CtaSmem {
 
 // Per-warp shared-memory block of the stream kernel (offsets from its base):
 // [ring: kStages x 4 KiB][stash][group thread values][mbarriers], 128-aligned.
-template <typename F>
+// UNAL: the ring of the unaligned-vector stream kernel: a stage holds the
+// 16-byte-aligned span around its batch (4 KiB + 16 bytes).
+template <typename F, bool UNAL = false>
 struct WarpSmem {
+  static constexpr uint32_t kStage = UNAL ? kBatchBytes + 16 : kBatchBytes;
   static constexpr uint32_t kRing = 0;
-  static constexpr uint32_t kStash = kStages * kBatchBytes;
+  static constexpr uint32_t kStash = kStages * kStage;
   static constexpr uint32_t kXs = kStash + kStashBytes<F>;
   static constexpr uint32_t kBars = kXs + kGroupXsBytes<F>;
   static constexpr uint32_t kBytes = (kBars + kStages * 8 + 127) / 128 * 128;
 };
-static_assert(kWarps * WarpSmem<double>::kBytes + CtaSmem<double>::kBytes <= 227 * 1024 &&
-                  kWarps * WarpSmem<float>::kBytes + CtaSmem<float>::kBytes <= 227 * 1024,
+static_assert(kWarps * WarpSmem<double, true>::kBytes + CtaSmem<double>::kBytes <= 227 * 1024 &&
+                  kWarps * WarpSmem<float, true>::kBytes + CtaSmem<float>::kBytes <= 227 * 1024,
               "stream kernel shared memory");
 
 // Stream loader (contiguous tiles: a vector, or back-to-back columns of T
@@ -598,12 +604,19 @@ static_assert(kWarps * WarpSmem<double>::kBytes + CtaSmem<double>::kBytes <= 227
 // GAP: column blocks with a gap between columns (ld > rows, rows a multiple
 // of T, 16-byte aligned columns): the walk also skips (ld - rows) elements at
 // every column end, and a new group's start is computed from its tile index.
-template <typename F, bool GAP = false>
+// UNAL (vectors whose base is a multiple of sizeof(F) but not of 16 bytes,
+// the paper's unaligned case): a batch starting at byte offset
+// `off` = x mod 16 is fetched as the aligned span [B - off, B - off + 4 KiB
+// + 16), and the lanes read their rows `off` bytes into the stage with
+// element-sized shared loads.  The span stays inside the array because the
+// kernel streams only groups with a group before them (group >= 1) and at
+// least 16 bytes of the array after them (the others go through single_tile).
+template <typename F, bool GAP = false, bool UNAL = false>
 struct StreamLoader {
   static constexpr int BPI = 1;
   static constexpr bool kMaybePadding = false;
   __device__ __forceinline__ bool all_padding(int) const { return false; }
-  using L = WarpSmem<F>;
+  using L = WarpSmem<F, UNAL>;
 
   uint32_t my_s;         // this warp's block (WarpSmem)
   uint32_t consumed;     // stages consumed (warp-uniform)
@@ -621,6 +634,7 @@ struct StreamLoader {
   int64_t tpc, ld;       // tiles per column, leading dimension (kernel-uniform)
   const F* x;
   int g0;                // (kernel-uniform)
+  uint32_t off;          // UNAL only: x mod 16 in bytes (kernel-uniform)
 
   __device__ __forceinline__ void seek(int grp) {
     const int64_t tau = (int64_t)grp << g0;
@@ -632,8 +646,8 @@ struct StreamLoader {
   __device__ __forceinline__ void issue(uint32_t slot) {
     if (groups_left < 0) return;
     if ((threadIdx.x & 31) == 0)
-      bulk_load(my_s + L::kRing + slot * kBatchBytes, p_ptr, kBatchBytes, my_s + L::kBars + slot * 8,
-                stream_l2_policy());
+      bulk_load(my_s + L::kRing + slot * L::kStage, UNAL ? p_ptr - off : p_ptr, L::kStage,
+                my_s + L::kBars + slot * 8, stream_l2_policy());
     p_ptr += kBatchBytes;
     if (GAP && --col_left == 0) {
       col_left = col_batches;
@@ -666,9 +680,13 @@ struct StreamLoader {
     for (int v = 0; v < Cfg<F>::V; ++v) o[v] = F(1) + F(row * 7 + v) * F(1e-3) + F(consumed & 3);
     return;
 #endif
-    const uint32_t addr = my_s + L::kRing + (consumed % kStages) * kBatchBytes + (threadIdx.x & 31) * 16 +
-                          row * (kBatchBytes / kBatch);
-    if constexpr (sizeof(F) == 8) {
+    const uint32_t addr = my_s + L::kRing + (consumed % kStages) * L::kStage + (threadIdx.x & 31) * 16 +
+                          row * (kBatchBytes / kBatch) + (UNAL ? off : 0u);
+    if constexpr (UNAL) {
+      // element-aligned only: one shared load per element
+#pragma unroll
+      for (int v = 0; v < Cfg<F>::V; ++v) ld_shared(addr + v * (uint32_t)sizeof(F), o[v]);
+    } else if constexpr (sizeof(F) == 8) {
       double a0, a1;
       asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0), "=d"(a1) : "r"(addr) : "memory");
       o[0] = a0;
@@ -848,11 +866,15 @@ __device__ __forceinline__ void short_pair(const TreeJob<F>& job, int64_t tau, F
   }
 }
 
-template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false>
+template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false, bool UNAL = false>
 __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(const TreeJob<F> job) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr bool kPipe = TMA && NRMF_USE_TMA;
   constexpr bool kStream = kPipe && STREAM && NT == 1;
+  static_assert(!UNAL || (kStream && !GAP), "UNAL: the vector stream kernel only");
+  using WS = WarpSmem<F, UNAL>;
+  // tile loads outside the ring: 16-byte vectors unless the base is unaligned
+  constexpr LoadMode kTileMode = UNAL ? kScalar : kVec;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // group and warp indices are 32-bit (a call has < 2^31 tiles: n < 2^43);
   // fewer live 64-bit values leave more registers to the node chains
@@ -865,11 +887,19 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   const int n_groups = (int)((job.n_items + G - 1) >> job.g0);
   // stream mode: warp groups made only of full tiles (tiles are contiguous:
   // a vector, or columns with ld == rows == a multiple of T)
-  const int n_full = kStream ? (int)((job.ld == 0 ? job.len / kTile : job.n_items) >> job.g0) : 0;
+  int n_full = kStream ? (int)((job.ld == 0 ? job.len / kTile : job.n_items) >> job.g0) : 0;
+  // UNAL: the first streamed group is 1 (group 0's span would start before
+  // x), and the last full group is streamed only if at least 16 bytes of the
+  // array follow it (its last span ends 16 - off bytes past the group)
+  const uint32_t u_off = UNAL ? (uint32_t)(reinterpret_cast<uintptr_t>(job.x) & 15u) : 0u;
+  if (UNAL && n_full > 0 &&
+      (job.len - ((int64_t)n_full << job.g0) * kTile) * (int64_t)sizeof(F) < 16)
+    --n_full;
+  const int s_lo = UNAL ? 1 : 0;
 
-  StreamLoader<F, GAP> sl;
+  StreamLoader<F, GAP, UNAL> sl;
   if (kStream) {
-    using L = WarpSmem<F>;
+    using L = WS;
     sl.my_s = smem_u32(smem) + w * L::kBytes;
     if (lane == 0) {
       for (int st = 0; st < kStages; ++st) mbar_init(sl.my_s + L::kBars + st * 8, 1);
@@ -879,8 +909,10 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     sl.consumed = 0;
     sl.group_batches = G * (Cfg<F>::J / kBatch);
     sl.p_left = sl.group_batches;
-    // groups gw, gw + W, ... below n_full: this warp streams 1 + groups_left of them
-    sl.groups_left = gw < n_full ? (int)((n_full - 1 - gw) / W) : -1;
+    // groups gw, gw + W, ... in [s_lo, n_full): this warp streams 1 + groups_left of them
+    const int first = gw < s_lo ? gw + W : gw;
+    sl.groups_left = first < n_full ? (int)((n_full - 1 - first) / W) : -1;
+    sl.off = u_off;
     if (GAP) {
       sl.x = job.x;
       sl.tpc = job.tpc;
@@ -892,12 +924,12 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
       sl.p_grp = gw;
       if (sl.groups_left >= 0) sl.seek(gw);
     } else {
-      sl.p_ptr = reinterpret_cast<const char*>(job.x + gw * G * (int64_t)kTile);
+      sl.p_ptr = reinterpret_cast<const char*>(job.x + first * G * (int64_t)kTile);
       sl.skip_bytes = (W - 1) * G * (int64_t)kTile * (int64_t)sizeof(F);
     }
     for (int st = 0; st < kStages; ++st) sl.issue(st);
   }
-  const uint32_t cta_s = smem_u32(smem) + kWarps * WarpSmem<F>::kBytes;
+  const uint32_t cta_s = smem_u32(smem) + kWarps * WS::kBytes;
   if (kStream && job.cta_step0) {
     if (threadIdx.x < kCtaSlots) {
       st_shared_u32(cta_s + CtaSmem<F>::kCnt + threadIdx.x * 4, 0u);
@@ -932,19 +964,47 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   }
 
   NRMF_TRACE(0, 0, 0);
+  // safe mode (stream kernel): after a group that needed the exact path, the
+  // warp evaluates its next groups with the safe node straight from the ring
+  // (no fast pass to discard, no re-read from global memory) until a group
+  // whose leaves all lie in the fast domain.  Same tree, same bits.
+  bool safe_mode = false;
   for (int grp = gw, rnd = 0; grp < n_groups; grp += W, ++rnd) {
     F s0[1], s1[1], s2[1], gv[1];
     NodeTop ne{job.top_cr};
     bool group_done = false;
-    if (kStream && grp < n_full) {
+#if NRMF_SAFE_MODE
+    if (kStream && safe_mode && grp >= s_lo && grp < n_full) {
+      NodeSafeChk node;
+      const uint32_t xs = sl.my_s + WS::kXs;
+      for (int k = 0; k < G; ++k) {  // rolled
+        F c = warp_tile_lanes<F>(sl, node, sl.my_s + WS::kStash);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) c = node(c, __shfl_xor_sync(0xffffffffu, c, off));
+        if (lane == 0) {
+          st_shared(xs + k * (uint32_t)sizeof(F), c);
+          if (job.tile_out != nullptr) job.tile_out[grp * G + k] = c;
+        }
+      }
+      __syncwarp();
+      F v = F(0);
+      if (lane < G) ld_shared(xs + lane * (uint32_t)sizeof(F), v);
+      __syncwarp();
+      for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
+      gv[0] = v;
+      group_done = true;
+      safe_mode = __any_sync(0xffffffffu, node.bad);
+    }
+#endif
+    if (kStream && !group_done && grp >= s_lo && grp < n_full) {
       // full warp group of a vector call: per tile the thread values go to
       // the warp's xs area, then the cross-thread and group levels of all G
       // tiles at once (group_cross).  A flagged leaf or a NaN tile value
       // recomputes the group with the exact path below.
       NodeFast node;
       for (int k = 0; k < G; ++k) {  // rolled
-        const F c = warp_tile_lanes<F>(sl, node, sl.my_s + WarpSmem<F>::kStash);
-        st_shared(sl.my_s + WarpSmem<F>::kXs + (k * 32 + lane) * (uint32_t)sizeof(F), c);
+        const F c = warp_tile_lanes<F>(sl, node, sl.my_s + WS::kStash);
+        st_shared(sl.my_s + WS::kXs + (k * 32 + lane) * (uint32_t)sizeof(F), c);
 #if NRMF_SKIP_FLAGGED
         // a flagged tile sends the whole group to the fallback: the group's
         // remaining batches are only drained from the ring, not evaluated
@@ -957,25 +1017,25 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
       __syncwarp();
 #ifdef NRMF_PROBE_NO_GROUPCROSS  // dev-only timing probe: no cross-thread/group levels (wrong results)
       if (!__any_sync(0xffffffffu, node.bad)) {
-        ld_shared(sl.my_s + WarpSmem<F>::kXs + lane * (uint32_t)sizeof(F), gv[0]);
+        ld_shared(sl.my_s + WS::kXs + lane * (uint32_t)sizeof(F), gv[0]);
         group_done = true;
       }
 #else
       if (!__any_sync(0xffffffffu, node.bad))
-        group_done = group_cross<F>(node, sl.my_s + WarpSmem<F>::kXs, G, job.top_cr, gv[0],
+        group_done = group_cross<F>(node, sl.my_s + WS::kXs, G, job.top_cr, gv[0],
                                     job.tile_out != nullptr ? job.tile_out + grp * G : nullptr);
 #endif
       if (!group_done) {
         // exact path: the G tile values through the xs area, then the lg G
         // group levels as a shuffle tree (contiguous pairs, the same tree)
-        const uint32_t xs = sl.my_s + WarpSmem<F>::kXs;
+        const uint32_t xs = sl.my_s + WS::kXs;
         for (int k = 0; k < G; ++k) {  // rolled
           const F* tb = job.x + (grp * G + k) * (int64_t)kTile;  // contiguous tiles
           if (GAP) {
             int64_t remv;
             tile_at(job, grp * G + k, tb, remv);  // a full tile of a gapped column block
           }
-          const F tv = warp_tile_exact<F, kVec>(tb, kTile);
+          const F tv = warp_tile_exact<F, kTileMode>(tb, kTile);
           if (lane == 0) {
             st_shared(xs + k * (uint32_t)sizeof(F), tv);
             if (job.tile_out != nullptr) job.tile_out[grp * G + k] = tv;
@@ -988,6 +1048,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
         gv[0] = v;
         group_done = true;
+        safe_mode = true;
       }
     }
     // short columns (every tile one column of rows <= 2 batches): two
@@ -1026,7 +1087,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
           if (bad || tv[t] != tv[t]) tv[t] = warp_tile_exact<F, kVec>(bases[t], kTile);
       } else {
 #pragma unroll
-        for (int t = 0; t < NT; ++t) tv[t] = (k + t < G) ? single_tile<F, TMA>(job, grp * G + k + t) : F(0);
+        for (int t = 0; t < NT; ++t) tv[t] = (k + t < G) ? single_tile<F, TMA && !UNAL>(job, grp * G + k + t) : F(0);
       }
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
@@ -1035,7 +1096,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         if (job.tile_out != nullptr && lane == 0 && tau < job.n_items) job.tile_out[tau] = tv[t];
         gv[0] = tv[t];
         if (kStream) {
-          if (lane == 0) st_shared(sl.my_s + WarpSmem<F>::kXs + (k + t) * (uint32_t)sizeof(F), tv[t]);
+          if (lane == 0) st_shared(sl.my_s + WS::kXs + (k + t) * (uint32_t)sizeof(F), tv[t]);
           continue;
         }
         if (G == 8) counter_merge<F, 1, 8>(k + t, gv, s0, s1, s2, ne);
@@ -1046,7 +1107,7 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     if (kStream && xs_merge) {
       __syncwarp();
       F v = F(0);
-      if (lane < G) ld_shared(sl.my_s + WarpSmem<F>::kXs + lane * (uint32_t)sizeof(F), v);
+      if (lane < G) ld_shared(sl.my_s + WS::kXs + lane * (uint32_t)sizeof(F), v);
       __syncwarp();
       for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
       gv[0] = v;
@@ -1370,17 +1431,17 @@ static void set_exchange(TreeJob<F>& job, const RankExchange* rx) {
 
 // Dynamic shared memory: stream kernel kWarps x WarpSmem; column (PipeLoader)
 // kernel [ring: kWarps x kStages x 4 KiB][barriers].
-template <typename F, bool TMA, bool STREAM = false>
+template <typename F, bool TMA, bool STREAM = false, bool UNAL = false>
 static size_t kernel_smem() {
   if (!(TMA && NRMF_USE_TMA)) return 0;
-  if (STREAM) return (size_t)kWarps * WarpSmem<F>::kBytes + CtaSmem<F>::kBytes;
+  if (STREAM) return (size_t)kWarps * WarpSmem<F, UNAL>::kBytes + CtaSmem<F>::kBytes;
   return (size_t)kWarps * kStages * kBatchBytes + (size_t)kWarps * kStages * 8;
 }
 
 // Function attributes (the dynamic shared memory opt-in) belong to a device's
 // context: they are set, and the occupancy cached, once per device.
 constexpr int kMaxDevices = 64;
-template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false>
+template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false, bool UNAL = false>
 static int blocks_per_sm() {
   static std::atomic<int> cached[kMaxDevices];
   static std::mutex mu;
@@ -1392,11 +1453,12 @@ static int blocks_per_sm() {
   std::lock_guard<std::mutex> lock(mu);
   b = cached[dev].load(std::memory_order_relaxed);
   if (b != 0) return b;
-  const size_t sm = kernel_smem<F, TMA, STREAM>();
+  const size_t sm = kernel_smem<F, TMA, STREAM, UNAL>();
   if (sm > 48 * 1024)
-    cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM, GAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM, GAP>, kThreads, sm) !=
+    cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM, GAP, UNAL>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM, GAP, UNAL>, kThreads,
+                                                    sm) !=
           cudaSuccess ||
       b < 1)
     b = 1;
@@ -1409,6 +1471,7 @@ static int g_g0_override = -1;   // dev hook: force the warp-group level count g
 static int g_cta_step0 = NRMF_CTA_STEP;  // dev hook: first combine step in shared memory (stream kernel)
 static int g_gap_stream = 1;     // test hook: gapped column blocks on the stream kernel (0: general kernel)
 static int g_split_ll = 1;       // test hook: the split kernel's last step by slots (0: by a counter)
+static int g_unal_stream = 1;    // test hook: unaligned vectors on the stream kernel (0: element-load kernel)
 
 // Launch the tree kernel over items (tiles) with mapping (tpc, ld, len).
 template <typename F>
@@ -1426,8 +1489,12 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   // column blocks with gaps (ld > rows, rows a multiple of T; vec implies
   // 16-byte aligned columns): the stream kernel with the gap-skipping walk
   const bool gap = vec && g_gap_stream && ld > len && len % kTile == 0;
-  int64_t grid = (int64_t)device_sms() * (gap      ? blocks_per_sm<F, true, 1, true, true>()
-                                          : stream ? blocks_per_sm<F, true, 1, true>()
+  // a vector whose base is element- but not 16-byte aligned (the paper's
+  // unaligned case): the stream kernel with shifted spans (StreamLoader UNAL)
+  const bool ustream = !vec && ld == 0 && g_unal_stream;
+  int64_t grid = (int64_t)device_sms() * (gap       ? blocks_per_sm<F, true, 1, true, true>()
+                                          : stream  ? blocks_per_sm<F, true, 1, true>()
+                                          : ustream ? blocks_per_sm<F, true, 1, true, false, true>()
                                           : vec  ? blocks_per_sm<F, true, NRMF_NT, false>()
                                                  : blocks_per_sm<F, false, 1, false>());
   if (g_grid_override > 0) grid = g_grid_override;
@@ -1476,7 +1543,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   int g0_max = 0;
   // groups of up to kMaxGroup tiles on the stream kernel, 8 elsewhere
   // (the column kernel's counter merge has three levels)
-  const int gmax = (stream || gap) ? (sizeof(F) == 4 ? 4 : 3) : 3;
+  const int gmax = (stream || gap || ustream) ? (sizeof(F) == 4 ? 4 : 3) : 3;
   {
     const int64_t W = grid * kWarps;
     double best = 0.0;
@@ -1497,7 +1564,7 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   Plan pl = combine ? make_plan(n_items, p2, g0_max)
                     : make_plan(n_items, int64_t(1) << g0_max, g0_max);
   bool cta_step0 = false;
-  if ((stream || gap) && combine && kWarps == 16 && g_cta_step0 &&
+  if ((stream || gap || ustream) && combine && kWarps == 16 && g_cta_step0 &&
       ((n_items + (int64_t(1) << pl.g0) - 1) >> pl.g0) >= grid * kWarps) {
     const Plan p4 = make_plan(n_items, p2, g0_max, 4);
     if (p4.nsteps >= 1 && p4.lg_fan[0] == 4 && p4.g0 == pl.g0) {
@@ -1525,6 +1592,9 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
     nrmf_tree_kernel<F, true, 1, true, true><<<(unsigned)grid, kThreads, kernel_smem<F, true, true>(), s>>>(job);
   } else if (stream) {
     nrmf_tree_kernel<F, true, 1, true><<<(unsigned)grid, kThreads, kernel_smem<F, true, true>(), s>>>(job);
+  } else if (ustream) {
+    nrmf_tree_kernel<F, true, 1, true, false, true>
+        <<<(unsigned)grid, kThreads, kernel_smem<F, true, true, true>(), s>>>(job);
   } else if (vec && pl.g0 >= 1 && NRMF_NT == 2) {
     blocks_per_sm<F, true, NRMF_NT, false>();
     nrmf_tree_kernel<F, true, NRMF_NT, false><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
@@ -1882,6 +1952,11 @@ int nrmf_debug_set_g0(int g0) {
 
 int nrmf_debug_set_gap_stream(int on) {
   g_gap_stream = on != 0;
+  return NRMF_OK;
+}
+
+int nrmf_debug_set_unal_stream(int on) {
+  g_unal_stream = on != 0;
   return NRMF_OK;
 }
 
