@@ -764,16 +764,24 @@ def other_configs(nrmf, device, stream, hbm_peak):
                  "bit_exact_vs_oracle": bool(o1.cpu().numpy().tobytes() == np.float64(oracle.nrmf(x1h)).tobytes())}
     del x1, flush
     # the paper's unaligned case (aligned vs unaligned loads): a base
-    # 8 bytes past a 16-byte boundary takes the element-load path (same bits)
+    # 8 bytes past a 16-byte boundary runs the stream kernel on shifted spans
+    # (StreamLoader UNAL; same bits); the element-load kernel beside it
     nu = 1 << 28
     xuh = gen.normal(2, nu + 1)
     xu = torch.from_numpy(xuh).to(device)
     ou = torch.empty((), dtype=torch.float64, device=device)
     xa, xm = xu[:nu], xu[1:]
     msa = timed(lambda: nrmf.norm(xa, out=ou))
+    try:
+        nrmf._debug_set_unal_stream(False)
+        mse = timed(lambda: nrmf.norm(xm, out=ou))
+    finally:
+        nrmf._debug_set_unal_stream(True)
     msu = timed(lambda: nrmf.norm(xm, out=ou))
     res["unaligned"] = {"workload": "DNRMF fp64 n=2^28 N(0,1), base 16-byte aligned vs 8 bytes off",
                         "ms_aligned": round(msa, 4), "ms_unaligned": round(msu, 4),
+                        "unaligned_frac_of_aligned": round(msa / msu, 3),
+                        "ms_unaligned_element_loads": round(mse, 4),
                         "GB/s_aligned": round(nu * 8 / (msa * 1e-3) / 1e9, 1),
                         "GB/s_unaligned": round(nu * 8 / (msu * 1e-3) / 1e9, 1),
                         "bit_exact_vs_oracle": bool(ou.cpu().numpy().tobytes() ==

@@ -31,7 +31,7 @@ namespace nrmf {
 constexpr int kMaxSteps = 8;
 constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's last one up to 8 (fan-in 256)
 #ifndef NRMF_SAFE_MODE
-#define NRMF_SAFE_MODE 0      // stream kernel: safe-node groups from the ring after a flagged group
+#define NRMF_SAFE_MODE 1      // stream kernel: safe-node groups from the ring after a flagged group
 #endif
 #ifndef NRMF_STAGES
 #define NRMF_STAGES 2         // TMA ring depth per warp (batches of 4 KiB)
@@ -752,7 +752,7 @@ __device__ __forceinline__ void fence_acq_rel_cta() { asm volatile("fence.acq_re
 // Claim round rr's slot if complete and unclaimed; if claimed, evaluate CTA
 // block b and announce it to step 1 (climbing if last there).
 template <typename F>
-__device__ void cta_try(const TreeJob<F>& job, uint32_t cta_s, int rr, int b, int n_groups) {
+__device__ __forceinline__ void cta_try(const TreeJob<F>& job, uint32_t cta_s, int rr, int b, int n_groups) {
   using C = CtaSmem<F>;
   const int lane = threadIdx.x & 31;
   const uint32_t slot = (uint32_t)rr & (kCtaSlots - 1);
@@ -968,35 +968,15 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
   // warp evaluates its next groups with the safe node straight from the ring
   // (no fast pass to discard, no re-read from global memory) until a group
   // whose leaves all lie in the fast domain.  Same tree, same bits.
+  // (fp64 only: C5 is an fp64 config, and the fp32 kernel's hot loop lost
+  // 2 % to the extra code)
+  constexpr bool kSafeMode = NRMF_SAFE_MODE && kStream && sizeof(F) == 8;
   bool safe_mode = false;
   for (int grp = gw, rnd = 0; grp < n_groups; grp += W, ++rnd) {
     F s0[1], s1[1], s2[1], gv[1];
     NodeTop ne{job.top_cr};
     bool group_done = false;
-#if NRMF_SAFE_MODE
-    if (kStream && safe_mode && grp >= s_lo && grp < n_full) {
-      NodeSafeChk node;
-      const uint32_t xs = sl.my_s + WS::kXs;
-      for (int k = 0; k < G; ++k) {  // rolled
-        F c = warp_tile_lanes<F>(sl, node, sl.my_s + WS::kStash);
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) c = node(c, __shfl_xor_sync(0xffffffffu, c, off));
-        if (lane == 0) {
-          st_shared(xs + k * (uint32_t)sizeof(F), c);
-          if (job.tile_out != nullptr) job.tile_out[grp * G + k] = c;
-        }
-      }
-      __syncwarp();
-      F v = F(0);
-      if (lane < G) ld_shared(xs + lane * (uint32_t)sizeof(F), v);
-      __syncwarp();
-      for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
-      gv[0] = v;
-      group_done = true;
-      safe_mode = __any_sync(0xffffffffu, node.bad);
-    }
-#endif
-    if (kStream && !group_done && grp >= s_lo && grp < n_full) {
+    if (kStream && !(kSafeMode && safe_mode) && grp >= s_lo && grp < n_full) {
       // full warp group of a vector call: per tile the thread values go to
       // the warp's xs area, then the cross-thread and group levels of all G
       // tiles at once (group_cross).  A flagged leaf or a NaN tile value
@@ -1048,8 +1028,31 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
         for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
         gv[0] = v;
         group_done = true;
-        safe_mode = true;
+        if constexpr (kSafeMode) safe_mode = true;
       }
+    }
+    if constexpr (kSafeMode) {
+    if (safe_mode && !group_done && grp >= s_lo && grp < n_full) {
+      NodeSafeChk node;
+      const uint32_t xs = sl.my_s + WS::kXs;
+      for (int k = 0; k < G; ++k) {  // rolled
+        F c = warp_tile_lanes<F>(sl, node, sl.my_s + WS::kStash);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) c = node(c, __shfl_xor_sync(0xffffffffu, c, off));
+        if (lane == 0) {
+          st_shared(xs + k * (uint32_t)sizeof(F), c);
+          if (job.tile_out != nullptr) job.tile_out[grp * G + k] = c;
+        }
+      }
+      __syncwarp();
+      F v = F(0);
+      if (lane < G) ld_shared(xs + lane * (uint32_t)sizeof(F), v);
+      __syncwarp();
+      for (int off = 1; off < G; off <<= 1) v = top_node(v, __shfl_xor_sync(0xffffffffu, v, off), job.top_cr);
+      gv[0] = v;
+      group_done = true;
+      safe_mode = __any_sync(0xffffffffu, node.bad);
+    }
     }
     // short columns (every tile one column of rows <= 2 batches): two
     // columns at a time (warp_tiles_short2), merged like the loop below
