@@ -66,6 +66,10 @@ __device__ __forceinline__ void trace(unsigned type, unsigned level, unsigned id
   if ((threadIdx.x & 31) != 0 || g_trace == nullptr) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+#ifdef NRMF_PROBE_TRACE2  // one slot per (warp, event type): no atomics (split-kernel timelines)
+  if (type < 16) g_trace[((unsigned long long)blockIdx.x * 32 + (threadIdx.x >> 5)) * 16 + type] = t;
+  return;
+#endif
   const unsigned i = atomicAdd(&g_trace_n, 1u);
   if (i < g_trace_cap) {
     g_trace[2 * i] = ((unsigned long long)type << 56) | ((unsigned long long)level << 48) |
@@ -73,9 +77,31 @@ __device__ __forceinline__ void trace(unsigned type, unsigned level, unsigned id
     g_trace[2 * i + 1] = t;
   }
 }
+// an event with a time taken earlier (no atomic between the measured points)
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_at(unsigned type, unsigned long long t) {
+  if ((threadIdx.x & 31) != 0 || g_trace == nullptr) return;
+#ifdef NRMF_PROBE_TRACE2
+  if (type < 16) g_trace[((unsigned long long)blockIdx.x * 32 + (threadIdx.x >> 5)) * 16 + type] = t;
+  return;
+#endif
+  const unsigned i = atomicAdd(&g_trace_n, 1u);
+  if (i < g_trace_cap) {
+    g_trace[2 * i] = ((unsigned long long)type << 56) | ((unsigned long long)blockIdx.x << 24) | (threadIdx.x >> 5);
+    g_trace[2 * i + 1] = t;
+  }
+}
 #define NRMF_TRACE(a, b, c) trace(a, b, c)
+#define NRMF_TSTAMP(v) const unsigned long long v = gtime()
+#define NRMF_TRACE_AT(a, v) trace_at(a, v)
 #else
 #define NRMF_TRACE(a, b, c) (void)0
+#define NRMF_TSTAMP(v) (void)0
+#define NRMF_TRACE_AT(a, v) (void)0
 #endif
 
 #ifdef NRMF_PROBE_JITTER  // test build only: random delays at every step of the combine protocols
@@ -310,7 +336,7 @@ __device__ __forceinline__ void ll_store(const TreeJob<F>& job, int64_t i, F v, 
   if ((threadIdx.x & 31) == 0) {
     uint32_t lo, hi;
     to_words(v, lo, hi);
-    st_ll2(job.ll + 16 * (i + 1), lo, hi, (uint32_t)tag, (uint32_t)(tag >> 32));
+    st_ll2_gpu(job.ll + 16 * (i + 1), lo, hi, (uint32_t)tag, (uint32_t)(tag >> 32));
   }
 }
 // KP inputs per lane (lanes < 2^f when f <= 5): poll, then the fast tree with
@@ -327,21 +353,40 @@ __device__ __noinline__ F ll_gather_combine(char* ll, int64_t nin, int f, int cr
     a[j] = F(0);
     ready[j] = !(i < nin && (KP > 1 || lane < (1 << f)));
   }
+  // the lane's last slot index in range (slots past the inputs are re-read
+  // harmlessly: their results are ignored)
+  const int64_t i_last = nin - 1 < (int64_t)lane * KP ? nin - 1 : (int64_t)lane * KP + KP - 1;
   for (long long spins = 0;; ++spins) {
+    // every slot of the lane is loaded in one round, all loads issued before
+    // the first compare: one L2 round trip per round, not KP dependent ones
+    uint32_t lo[KP], e0[KP], hi[KP], e1[KP];
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      const int64_t i = (int64_t)lane * KP + j;
+      ld_ll_gpu(ll + 16 * ((i < i_last ? i : i_last) + 1), lo[j], e0[j], hi[j], e1[j]);
+    }
     bool all = true;
 #pragma unroll
     for (int j = 0; j < KP; ++j) {
       if (ready[j]) continue;
-      uint32_t lo, e0, hi, e1;
-      ld_ll(ll + 16 * ((int64_t)lane * KP + j + 1), lo, e0, hi, e1);
-      if (e0 == t1 && e1 == t2) {
-        a[j] = from_words<F>(lo, hi);
+      if (e0[j] == t1 && e1[j] == t2) {
+        a[j] = from_words<F>(lo[j], hi[j]);
         ready[j] = true;
       } else {
         all = false;
       }
     }
-    if (__all_sync(0xffffffffu, all)) break;
+#ifdef NRMF_PROBE_TRACE2
+    if (spins == 0) NRMF_TRACE(3, 0, 0);  // first poll round done
+    if (spins == 1) NRMF_TRACE(2, 0, 0);  // second
+#endif
+    if (__all_sync(0xffffffffu, all)) {
+#ifdef NRMF_PROBE_TRACE2
+      if ((threadIdx.x & 31) == 0 && g_trace != nullptr)
+        g_trace[((unsigned long long)blockIdx.x * 32 + (threadIdx.x >> 5)) * 16 + 7] = (unsigned long long)spins + 1;
+#endif
+      break;
+    }
     if (spins > (1ll << 26)) {  // never: every producer of the step writes its slot
 #pragma unroll
       for (int j = 0; j < KP; ++j)
@@ -350,25 +395,33 @@ __device__ __noinline__ F ll_gather_combine(char* ll, int64_t nin, int f, int cr
     }
     if (spins > 32) __nanosleep(32);
   }
+  NRMF_TSTAMP(t_polled);
   // clear the slots read: a later call with this layout whose call number
   // repeats (header reset by another call sharing the workspace) finds no
   // stale match
 #pragma unroll
   for (int j = 0; j < KP; ++j) {
     const int64_t i = (int64_t)lane * KP + j;
-    if (i < nin && (KP > 1 || lane < (1 << f))) st_ll2(ll + 16 * (i + 1), 0u, 0u, 0u, 0u);
+    if (i < nin && (KP > 1 || lane < (1 << f))) st_ll2_gpu(ll + 16 * (i + 1), 0u, 0u, 0u, 0u);
   }
   const int lv = f < 5 ? f : 5;
   bool bad = cr != 0;
   F v;
+  NRMF_TSTAMP(t_cleared);
   if (!bad) {
     F b[KP];
 #pragma unroll
     for (int j = 0; j < KP; ++j) b[j] = a[j];
     in_lane_levels<F, KP>(b, bad);
     v = b[0];
+    NRMF_TSTAMP(t_inlane);
     for (int l = 0; l < lv; ++l) v = v1h_fast<true>(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), bad);
     bad = __any_sync(0xffffffffu, lane < (1 << lv) && (bad || v != v));
+    NRMF_TSTAMP(t_shfl);
+    NRMF_TRACE_AT(10, t_polled);
+    NRMF_TRACE_AT(11, t_cleared);
+    NRMF_TRACE_AT(12, t_inlane);
+    NRMF_TRACE_AT(13, t_shfl);
   }
   if (bad) {
 #pragma unroll
@@ -1185,6 +1238,10 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     ld.tb = tb;
     ld.valid = kTile;
     ld.begin(it);
+#ifdef NRMF_PROBE_TRACE2  // the batch's loads have landed (the compare waits on them)
+    if (ld.u[kBatch - 1][V - 1] == F(-1234.5)) s_bad = 2;
+    NRMF_TRACE(14, 0, 0);
+#endif
     F r[V];
     batch_lanes<F>(ld, node, r);
     st_stash(smem_u32(stash) + ((k * NIT + it) * 32 + lane) * 16, r);
@@ -1192,6 +1249,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     NRMF_TRACE(5, 0, 0);
   }
   __syncthreads();
+  NRMF_TRACE(15, 0, 0);
   if (ll_comb) {
     ll_combine(job, ll_c);
     return;

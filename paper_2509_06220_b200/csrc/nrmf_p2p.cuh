@@ -54,6 +54,17 @@ __device__ __forceinline__ void ld_ll(const char* p, uint32_t& lo, uint32_t& e0,
   asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(lo), "=r"(e0), "=r"(hi), "=r"(e1)
                : "l"(p) : "memory");
 }
+// GPU-scope forms for slots read on the same device (the split kernel's last
+// step): strong .gpu loads and stores stay in this GPU's L2 coherence domain
+// (the .sys-scope volatile forms above are for peer memory)
+__device__ __forceinline__ void st_ll2_gpu(char* p, uint32_t lo, uint32_t hi, uint32_t e0, uint32_t e1) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(lo), "r"(e0), "r"(hi), "r"(e1)
+               : "memory");
+}
+__device__ __forceinline__ void ld_ll_gpu(const char* p, uint32_t& lo, uint32_t& e0, uint32_t& hi, uint32_t& e1) {
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(lo), "=r"(e0), "=r"(hi), "=r"(e1)
+               : "l"(p) : "memory");
+}
 __device__ __forceinline__ void to_words(double v, uint32_t& lo, uint32_t& hi) {
   lo = (uint32_t)__double2loint(v);
   hi = (uint32_t)__double2hiint(v);

@@ -57,7 +57,8 @@ def main():
         t = (a[:, 1] - a[:, 1].min()).astype(np.int64) / 1e3  # us
         print(f"== {dt} n=2^{lg}: event-timed {ms * 1e3:.1f} us, {len(a)} events")
         for k, name in ((0, "start"), (5, "batch end"), (1, "group end"), (9, "ll store"), (2, "climb start"),
-                        (3, "climb end"), (6, "ll poll start"), (8, "ll root"), (4, "exit")):
+                        (3, "climb end"), (6, "ll poll start"), (10, "ll polled"), (11, "ll cleared"),
+                        (12, "ll in-lane"), (13, "ll shuffles"), (8, "ll root"), (4, "exit")):
             tk = t[typ == k]
             if len(tk):
                 print(f"  {name:12s} n={len(tk):6d} min {tk.min():8.1f} med {np.median(tk):8.1f} "
