@@ -150,6 +150,28 @@ def make_input(config: str, n: int, off: int, dt):
     raise ValueError(config)
 
 
+def _nvtx(name):
+    """NVTX range around a bench phase (visible in nsys / ncu --nvtx; host-side
+    push/pop outside the event-timed regions, no cost to the device times)."""
+    def deco(fn):
+        def wrapped(*a, **k):
+            import torch
+            try:
+                torch.cuda.nvtx.range_push(name)
+                pushed = True
+            except Exception:  # no NVTX in this build of torch: time without the range
+                pushed = False
+            try:
+                return fn(*a, **k)
+            finally:
+                if pushed:
+                    torch.cuda.nvtx.range_pop()
+        wrapped.__name__, wrapped.__doc__ = fn.__name__, fn.__doc__
+        return wrapped
+    return deco
+
+
+@_nvtx("nrmf.bench.burst")
 def burst_point(step, stream, total_bytes, hbm_peak, local, flush=None):
     import torch
     ts = []
@@ -173,6 +195,7 @@ def burst_point(step, stream, total_bytes, hbm_peak, local, flush=None):
             "note": "after ~15 s idle (CPU oracle); context only, not the line's value"}
 
 
+@_nvtx("nrmf.bench.sustained")
 def sustained_point(step, stream, total_bytes, hbm_peak, local, flush=None, launches=300):
     """Context: the step launched `launches` times back to back
     right after the burst point, each launch timed by its own events; the
@@ -216,6 +239,7 @@ def golden_hex(config):
     return None
 
 
+@_nvtx("nrmf.bench.timed_steps")
 def time_loop(fn, steps: int, stream, flush=None):
     import torch
     if flush is not None:
@@ -727,6 +751,7 @@ def sumsq_context(x, ex, dt, ms_nrmf, args, stream):
             "ulp": ulp_distance(v, ex, dt)}
 
 
+@_nvtx("nrmf.bench.other_configs")
 def other_configs(nrmf, device, stream, hbm_peak):
     """The other BASELINE configs, reported beside the metric (parity-test
     cases, not bench lines): C1 DNRMF n=2^20 (cold and L2-resident), C2 SNRMF
@@ -759,9 +784,40 @@ def other_configs(nrmf, device, stream, hbm_peak):
         g1.replay()
     ms_cold = time_loop(g1.replay, 50, stream, flush)
     ms_warm = time_loop(g1.replay, 50, stream)
+
+    # Per-call event pairs behind a 256 MiB flush carry a fixed overhead and
+    # move in ~2.05 us steps on this pool (a 1 us globaltimer spin kernel
+    # timed the same way reads 6.1 us; tools/timer_probe.py).  So also: the
+    # call's cost inside a stream, by difference of two long sequences timed
+    # with one event pair each, K x [flush; call] - K x [flush], and the same
+    # for an empty kernel (the launch gap every kernel pays).
+    def seq_us(body, k=200):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            body()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / k
+
+    tiny = torch.zeros(1, device=device)
+    d_call, d_empty = [], []
+    for _ in range(3):
+        t_f = seq_us(flush.zero_)
+        d_call.append(seq_us(lambda: (flush.zero_(), g1.replay())) - t_f)
+        d_empty.append(seq_us(lambda: (flush.zero_(), tiny.add_(0))) - t_f)
+    floor = time_loop(lambda: tiny.add_(0), 50, stream, flush)
     res["C1"] = {"workload": "DNRMF fp64 n=2^20 U[-1,1)", "us_cold_l2_flushed": round(ms_cold * 1e3, 2),
+                 "us_cold_by_difference": round(float(np.median(d_call)), 2),
+                 "us_empty_kernel_by_difference": round(float(np.median(d_empty)), 2),
+                 "us_empty_kernel_per_call_events": round(floor * 1e3, 2),
+                 "note": "us_cold_l2_flushed: one event pair per call behind the flush (includes the event "
+                         "floor us_empty_kernel_per_call_events); us_cold_by_difference: median over 3 of "
+                         "(200 x [flush; call] - 200 x [flush]) / 200, one event pair per sequence",
                  "us_warm_l2_resident": round(ms_warm * 1e3, 2), "graph_nodes": 1,
                  "bit_exact_vs_oracle": bool(o1.cpu().numpy().tobytes() == np.float64(oracle.nrmf(x1h)).tobytes())}
+    del tiny
     del x1, flush
     # the paper's unaligned case (aligned vs unaligned loads): a base
     # 8 bytes past a 16-byte boundary runs the stream kernel on shifted spans

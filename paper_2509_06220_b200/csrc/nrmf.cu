@@ -1210,16 +1210,17 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   static_assert(kSplitWarps % NIT == 0, "whole tiles per CTA");
   __shared__ __align__(16) unsigned char stash[kSplitWarps * 32 * 16];  // [tile k][batch it][thread]
   __shared__ __align__(16) F xs[kSplitWarps / NIT * 32];
-  __shared__ int s_bad;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = 1 << job.g0;
   const int64_t grp = blockIdx.x;
   const int k = w / NIT, it = w % NIT;
   NRMF_TRACE(0, 0, 0);
   const bool ll_comb = job.ll != nullptr && blockIdx.x == 0 && w == 1;
-  // this call's number (the combiner) and slot tag (the producers: warp 0s)
-  const uint64_t ll_c = (job.ll != nullptr && (w == 0 || ll_comb)) ? ll_call(job) : 0ull;
-  const uint64_t ll_t = job.ll != nullptr && w == 0 ? ll_tag(job.ll, ll_c) : 0ull;
+  // this call's number (the combiner; the producers' slot tag is hashed from
+  // it after the batch phase): the header load -- a DRAM round trip with a
+  // cold L2 -- is issued behind the batch loads, not ahead of them
+  const bool need_hdr = job.ll != nullptr && (w == 0 || ll_comb);
+  uint64_t ll_c = 0;
   // are all G tiles of the group full tiles with data?
   bool full = (grp + 1) * G <= job.n_items;
   for (int t = 0; t < G && full; ++t) {
@@ -1227,8 +1228,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     int64_t remv;
     full = tile_at(job, grp * G + t, tb, remv);
   }
-  if (threadIdx.x == 0) s_bad = 0;
-  __syncthreads();
+  bool flagged = false;
   if (full && k < G) {
     NodeFast node;
     GlobalLoader<F, MODE> ld;
@@ -1238,17 +1238,22 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     ld.tb = tb;
     ld.valid = kTile;
     ld.begin(it);
+    if (need_hdr) ll_c = ll_call(job);
 #ifdef NRMF_PROBE_TRACE2  // the batch's loads have landed (the compare waits on them)
-    if (ld.u[kBatch - 1][V - 1] == F(-1234.5)) s_bad = 2;
+    if (ld.u[kBatch - 1][V - 1] == F(-1234.5)) flagged = true;
     NRMF_TRACE(14, 0, 0);
 #endif
     F r[V];
     batch_lanes<F>(ld, node, r);
     st_stash(smem_u32(stash) + ((k * NIT + it) * 32 + lane) * 16, r);
-    if (__any_sync(0xffffffffu, node.bad) && lane == 0) s_bad = 1;
+    flagged |= node.bad;
     NRMF_TRACE(5, 0, 0);
+  } else if (need_hdr) {
+    ll_c = ll_call(job);
   }
-  __syncthreads();
+  // one barrier (no flag to clear before the loads): the stash is complete
+  // and every warp knows whether any batch of the CTA flagged a leaf
+  const bool any_bad = __syncthreads_or(flagged) != 0;
   NRMF_TRACE(15, 0, 0);
   if (ll_comb) {
     ll_combine(job, ll_c);
@@ -1257,7 +1262,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   if (w != 0) return;
   F gv = F(0);
   bool done = false;
-  if (full && s_bad == 0) {
+  if (full && !any_bad) {
     NodeFast node;
     for (int t = 0; t < G; ++t) {
       F u[NIT][V];
@@ -1289,6 +1294,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
     return;
   }
   NRMF_JITTER(11);
+  const uint64_t ll_t = job.ll != nullptr ? ll_tag(job.ll, ll_c) : 0ull;
   if (job.ll != nullptr && job.nsteps == 1) {  // the group is an input of the last step
     ll_store(job, grp, gv, ll_t);
     return;

@@ -1,7 +1,8 @@
 """Dev tool: C1-sized (and other small / unaligned) calls of several
 libnrmf.so builds, A/B on one box: each call captured in a CUDA graph (flags
 NRMF_WS_CLEAN, as bench.py's capture does), L2 flushed before every replay,
-median device time over rounds that interleave the builds.
+median device time over rounds that interleave the builds (by default by
+difference: reps x [flush; call] minus reps x [flush], see --diff).
 
     python tools/c1_ab.py lib1.so lib2.so ... [--lg 20] [--off 0] [--dtype d]"""
 import argparse
@@ -32,6 +33,10 @@ def main():
     ap.add_argument("--flush", type=int, default=1)
     ap.add_argument("--pad", type=int, default=0, help="KiB allocated before each workspace (address probe)")
     ap.add_argument("--wspad", type=int, default=0, help="extra KiB of workspace (layout probe)")
+    ap.add_argument("--diff", type=int, default=1,
+                    help="1: time reps x [flush; call] and reps x [flush] with one event pair each and report the "
+                         "difference per call (per-call event pairs behind a flush carry ~4 us of event overhead "
+                         "and ~2.05 us steps on this pool: tools/timer_probe.py); 0: per-call event pairs")
     a = ap.parse_args()
     dt = torch.float64 if a.dtype == "d" else torch.float32
     n = 1 << a.lg
@@ -58,8 +63,24 @@ def main():
         graphs.append((p, g, out, (ws, keep)))
         print(f"{p}: ws at {ws.data_ptr():#x} ({ws.numel()} B), out at {out.data_ptr():#x}, x at {x.data_ptr():#x}", flush=True)
     res = {p: [] for p in a.libs}
+
+    def seq(body):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.reps):
+            body()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / a.reps
+
     for _ in range(a.rounds):
         for p, g, out, _ in graphs:
+            if a.diff:
+                t_fc = seq(lambda g=g: (flush.zero_(), g.replay()))
+                t_f = seq(lambda: flush.zero_())
+                res[p].append(t_fc - t_f)
+                continue
             ts = []
             for _ in range(a.reps):
                 if a.flush:
