@@ -14,7 +14,8 @@ import paper_2509_06220_b200 as nrmf  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 300
 LAUNCH = "--launch" in sys.argv
-rng = np.random.default_rng(2026)
+SEED = next((int(a.split("=")[1]) for a in sys.argv if a.startswith("--seed=")), 2026)
+rng = np.random.default_rng(SEED)
 bad = 0
 for i in range(N):
     n = int(np.exp(rng.uniform(0, np.log(1 << 24))))
