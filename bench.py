@@ -451,6 +451,31 @@ def run_ours(args):
     flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=device) if small else None
     with ClockSampler(local) as clk:
         ms = time_loop(step, args.steps, stream, flush)
+    by_diff = None
+    if small:
+        # context for small calls (other_configs C1 note): the same
+        # step by difference of two long flushed sequences, one event pair each
+        def seq_us(body, k=200):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(k):
+                body()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) * 1e3 / k
+        if dist:
+            td.barrier()
+        d = []
+        for _ in range(3):
+            t_f = seq_us(flush.zero_)
+            d.append(seq_us(lambda: (flush.zero_(), step())) - t_f)
+        by_diff = float(np.median(d))
+        if dist:
+            tt = torch.tensor([by_diff], dtype=torch.float64, device=device)
+            allt = torch.zeros(world, dtype=torch.float64, device=device)
+            td.all_gather_into_tensor(allt, tt)
+            by_diff = max(allt.tolist())
     per_rank_ms = [ms]
     if dist:
         tt = torch.tensor([ms], dtype=torch.float64, device=device)
@@ -506,6 +531,7 @@ def run_ours(args):
                           else "input > 126 MB L2 (no flush needed)"),
                    "tree_version": nrmf.tree_version(), "seed": 1},
         "gpu_launches": launches_per_step * args.steps,
+        "us_per_step_by_difference": None if by_diff is None else round(by_diff, 2),
         "graph": graph is not None,
         "rank_exchange": ("p2p" if p2p else "nccl_allgather") if dist else None,
         "clocks": clocks,
