@@ -1256,6 +1256,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   const bool any_bad = __syncthreads_or(flagged) != 0;
   NRMF_TRACE(15, 0, 0);
   if (ll_comb) {
+    if (job.peers != nullptr) prefetch_exchange(job.peers, job.p_rank);  // it polls long before the root
     ll_combine(job, ll_c);
     return;
   }

@@ -79,6 +79,18 @@ __device__ __forceinline__ F from_words(uint32_t lo, uint32_t hi) {
   else return __uint_as_float(lo);
 }
 
+// Pull this rank's exchange buffer (epoch word, both slot halves) and the
+// peer-pointer array into L2 ahead of rank_exchange, whose reads of them are
+// otherwise dependent DRAM misses (pointer, then epoch) at the very end of the
+// call.  Called by a warp with idle time before it writes the root (the split
+// kernel's slot-polling warp).  Warp-collective; prefetches only, no ordering.
+__device__ __forceinline__ void prefetch_exchange(char* const* peers, int rank) {
+  const int lane = threadIdx.x & 31;
+  if (lane < 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(peers) + lane * 128));
+  const char* own = peers[rank];
+  if (lane * 128 < kP2PBytes) asm volatile("prefetch.global.L2 [%0];" ::"l"(own + lane * 128));
+}
+
 // Warp-collective (all 32 lanes).  Returns, in every lane, the balanced tree
 // over the first nr rank values (nr a power of two <= world: the ranks that
 // own part of the tile tree), with v1_hypot or cr_hypot (cr) at every node.
