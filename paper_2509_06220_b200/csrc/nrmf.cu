@@ -912,7 +912,8 @@ __device__ __forceinline__ void short_pair(const TreeJob<F>& job, int64_t tau, F
   }
   tile_at(job, tau + 1, tb1, remv);
   bool bad = false;
-  warp_tiles_short2<F>(tb0, tb1, (int)remv, bad, tv[0], tv[1]);
+  if (remv <= kBatch * Cfg<F>::LANES) warp_tiles_short2<F, true>(tb0, tb1, (int)remv, bad, tv[0], tv[1]);
+  else warp_tiles_short2<F, false>(tb0, tb1, (int)remv, bad, tv[0], tv[1]);
   if (bad || tv[0] != tv[0] || tv[1] != tv[1]) {
     tv[0] = warp_tile_exact<F, kPred>(tb0, (int)remv);
     tv[1] = warp_tile_exact<F, kPred>(tb1, (int)remv);

@@ -77,3 +77,33 @@ def test_short_columns_forced_grids(nrmf, grid):
             run(nrmf, 333, 99, 333, dt, seed=grid + 20)
     finally:
         nrmf._debug_set_grid(0)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_short_columns_identity_skip_edges(nrmf, dt):
+    """Columns of at most one batch of rows skip the nodes whose right subtree
+    is padding in every lane (v1(L, +0) = L).  Plant out-of-domain values and
+    NaN in the leaves those skipped nodes pass through (the last valid row of
+    lane 0, whose row partner is padding in every lane), one special per
+    column, and compare with the oracle: the skipped leaf must keep the fast
+    node's leaf check, and a NaN must still reach the exact path."""
+    p = 64 if dt == np.float64 else 128
+    a = 2 if dt == np.float64 else 4
+    fi = np.finfo(dt)
+    specials = [0.0, -0.0, np.nan, np.inf, -np.inf, fi.max, -fi.max / 3, fi.tiny / 8, fi.smallest_subnormal,
+                fi.tiny * 2, 1.0, -2.5]
+    for r in (1, 2, p - 1, p, p + 1, 2 * p + 1, 3 * p - 5, 4 * p + 2, 5 * p, 6 * p + 3, 7 * p + 1, 8 * p):
+        lda = -(-r // a) * a
+        c = 2 * len(specials) + 1
+        A = gen.colscaled_normal(r, r, c, ld=lda, dtype=dt)
+        jmax = -(-r // p)
+        row_last = jmax - 1                       # lane 0's last valid row
+        for k, sv in enumerate(specials):
+            A[k * lda + row_last * p] = sv        # lane 0, last valid row
+            A[(len(specials) + k) * lda + r - 1] = sv   # the column's last element
+        T = torch.from_numpy(A).cuda().as_strided((r, c), (1, lda))
+        col, fr = nrmf.cols(T)
+        ecol, efr = oracle.cols(A, r, c, lda)
+        got = col.cpu().numpy()
+        same = (got.tobytes() == ecol.tobytes()) or np.array_equal(got, ecol, equal_nan=True)
+        assert same, (r, np.nonzero(~((got == ecol) | (np.isnan(got) & np.isnan(ecol))))[0][:5])
