@@ -239,6 +239,21 @@ def golden_hex(config):
     return None
 
 
+def seq_us(body, stream, k=200):
+    """Device time per iteration of k back-to-back calls of body() (each may
+    include an L2 flush), one event pair around the whole sequence: used by
+    difference, seq(flush; call) - seq(flush), for small calls."""
+    import torch
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        body()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / k
+
+
 @_nvtx("nrmf.bench.timed_steps")
 def time_loop(fn, steps: int, stream, flush=None):
     import torch
@@ -455,21 +470,12 @@ def run_ours(args):
     if small:
         # context for small calls (other_configs C1 note): the same
         # step by difference of two long flushed sequences, one event pair each
-        def seq_us(body, k=200):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(k):
-                body()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            return e0.elapsed_time(e1) * 1e3 / k
         if dist:
             td.barrier()
         d = []
         for _ in range(3):
-            t_f = seq_us(flush.zero_)
-            d.append(seq_us(lambda: (flush.zero_(), step())) - t_f)
+            t_f = seq_us(flush.zero_, stream)
+            d.append(seq_us(lambda: (flush.zero_(), step()), stream) - t_f)
         by_diff = float(np.median(d))
         if dist:
             tt = torch.tensor([by_diff], dtype=torch.float64, device=device)
@@ -817,22 +823,12 @@ def other_configs(nrmf, device, stream, hbm_peak):
     # call's cost inside a stream, by difference of two long sequences timed
     # with one event pair each, K x [flush; call] - K x [flush], and the same
     # for an empty kernel (the launch gap every kernel pays).
-    def seq_us(body, k=200):
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(k):
-            body()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) * 1e3 / k
-
     tiny = torch.zeros(1, device=device)
     d_call, d_empty = [], []
     for _ in range(3):
-        t_f = seq_us(flush.zero_)
-        d_call.append(seq_us(lambda: (flush.zero_(), g1.replay())) - t_f)
-        d_empty.append(seq_us(lambda: (flush.zero_(), tiny.add_(0))) - t_f)
+        t_f = seq_us(flush.zero_, stream)
+        d_call.append(seq_us(lambda: (flush.zero_(), g1.replay()), stream) - t_f)
+        d_empty.append(seq_us(lambda: (flush.zero_(), tiny.add_(0)), stream) - t_f)
     floor = time_loop(lambda: tiny.add_(0), 50, stream, flush)
     res["C1"] = {"workload": "DNRMF fp64 n=2^20 U[-1,1)", "us_cold_l2_flushed": round(ms_cold * 1e3, 2),
                  "us_cold_by_difference": round(float(np.median(d_call)), 2),
