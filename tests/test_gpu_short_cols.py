@@ -48,7 +48,7 @@ def run(nrmf, r, c, ld, dt, top="v1", specials=False, seed=1):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
-@pytest.mark.parametrize("r", [1, 5, 64, 127, 500, 1000, 1024, 2048])
+@pytest.mark.parametrize("r", [1, 5, 64, 127, 500, 600, 900, 1000, 1024, 1500, 2048])
 def test_short_columns_parity(nrmf, dt, r):
     if dt == np.float64 and r > 1024:
         r = 1023
@@ -82,7 +82,8 @@ def test_short_columns_forced_grids(nrmf, grid):
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_short_columns_identity_skip_edges(nrmf, dt):
     """Columns of at most one batch of rows skip the nodes whose right subtree
-    is padding in every lane (v1(L, +0) = L).  Plant out-of-domain values and
+    is padding in every lane (v1(L, +0) = L); longer ones (to 15 rows of lane
+    0) run the plain path with the same plants.  Plant out-of-domain values and
     NaN in the leaves those skipped nodes pass through (the last valid row of
     lane 0, whose row partner is padding in every lane), one special per
     column, and compare with the oracle: the skipped leaf must keep the fast
@@ -92,7 +93,8 @@ def test_short_columns_identity_skip_edges(nrmf, dt):
     fi = np.finfo(dt)
     specials = [0.0, -0.0, np.nan, np.inf, -np.inf, fi.max, -fi.max / 3, fi.tiny / 8, fi.smallest_subnormal,
                 fi.tiny * 2, 1.0, -2.5]
-    for r in (1, 2, p - 1, p, p + 1, 2 * p + 1, 3 * p - 5, 4 * p + 2, 5 * p, 6 * p + 3, 7 * p + 1, 8 * p):
+    for r in (1, 2, p - 1, p, p + 1, 2 * p + 1, 3 * p - 5, 4 * p + 2, 5 * p, 6 * p + 3, 7 * p + 1, 8 * p,
+              8 * p + 1, 9 * p + 1, 10 * p, 11 * p + 7, 13 * p + 2, 14 * p + 1, 15 * p - 1, 15 * p):
         lda = -(-r // a) * a
         c = 2 * len(specials) + 1
         A = gen.colscaled_normal(r, r, c, ld=lda, dtype=dt)
