@@ -45,6 +45,9 @@ constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's l
 #ifndef NRMF_SHORT_PAIRS
 #define NRMF_SHORT_PAIRS 1    // columns of rows <= 2 batches: two per warp at a time
 #endif
+#ifndef NRMF_SHORT_PAIRS_ELEM
+#define NRMF_SHORT_PAIRS_ELEM 1  // ... also in the element-load kernel (unaligned column blocks)
+#endif
 #ifndef NRMF_SKIP_FLAGGED
 #define NRMF_SKIP_FLAGGED 0   // 1: stream kernel stops evaluating a group at its first flagged tile (C5 -6 %, DNRMF +1.3 %: off)
 #endif
@@ -920,7 +923,10 @@ __device__ __forceinline__ void short_pair(const TreeJob<F>& job, int64_t tau, F
   }
 }
 
-template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false, bool UNAL = false>
+// SHORT: the element-load kernel's instance for short column blocks (every
+// column one partial tile of <= 2 batches), with the paired-column path; the
+// plain element-load instance keeps its code.
+template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false, bool UNAL = false, bool SHORT = false>
 __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(const TreeJob<F> job) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr bool kPipe = TMA && NRMF_USE_TMA;
@@ -1109,10 +1115,12 @@ __global__ void __launch_bounds__(kThreads, NRMF_MIN_BLOCKS) nrmf_tree_kernel(co
     }
     }
     // short columns (every tile one column of rows <= 2 batches): two
-    // columns at a time (warp_tiles_short2), merged like the loop below
-    // (16-byte aligned column blocks only: in the element-load kernel, which
-    // also serves unaligned vectors, the extra path cost those 8 %)
-    if (TMA && !kStream && NRMF_SHORT_PAIRS && !group_done && job.tpc == 1 && job.ld != 0 && G >= 2 &&
+    // columns at a time (warp_tiles_short2: element loads, any alignment),
+    // merged like the loop below -- in the TMA column kernel and, for column
+    // blocks that are not 16-byte aligned, the element-load kernel's SHORT
+    // instance
+    if ((TMA || (SHORT && NRMF_SHORT_PAIRS_ELEM)) && !kStream && NRMF_SHORT_PAIRS && !group_done &&
+        job.tpc == 1 && job.ld != 0 && G >= 2 &&
         job.len <= 2 * kBatch * Cfg<F>::LANES) {
       for (int k = 0; k < G; k += 2) {  // rolled
         F tv[2];
@@ -1510,7 +1518,7 @@ static size_t kernel_smem() {
 // Function attributes (the dynamic shared memory opt-in) belong to a device's
 // context: they are set, and the occupancy cached, once per device.
 constexpr int kMaxDevices = 64;
-template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false, bool UNAL = false>
+template <typename F, bool TMA, int NT, bool STREAM, bool GAP = false, bool UNAL = false, bool SHORT = false>
 static int blocks_per_sm() {
   static std::atomic<int> cached[kMaxDevices];
   static std::mutex mu;
@@ -1524,9 +1532,9 @@ static int blocks_per_sm() {
   if (b != 0) return b;
   const size_t sm = kernel_smem<F, TMA, STREAM, UNAL>();
   if (sm > 48 * 1024)
-    cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM, GAP, UNAL>,
+    cudaFuncSetAttribute(nrmf_tree_kernel<F, TMA, NT, STREAM, GAP, UNAL, SHORT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM, GAP, UNAL>, kThreads,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nrmf_tree_kernel<F, TMA, NT, STREAM, GAP, UNAL, SHORT>, kThreads,
                                                     sm) !=
           cudaSuccess ||
       b < 1)
@@ -1561,11 +1569,15 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   // a vector whose base is element- but not 16-byte aligned (the paper's
   // unaligned case): the stream kernel with shifted spans (StreamLoader UNAL)
   const bool ustream = !vec && ld == 0 && g_unal_stream;
+  // short column blocks that are not 16-byte aligned: the element-load
+  // kernel's SHORT instance (paired columns)
+  const bool eshort = !vec && !ustream && ld != 0 && tpc == 1 && len <= 2 * kBatch * Cfg<F>::LANES;
   int64_t grid = (int64_t)device_sms() * (gap       ? blocks_per_sm<F, true, 1, true, true>()
                                           : stream  ? blocks_per_sm<F, true, 1, true>()
                                           : ustream ? blocks_per_sm<F, true, 1, true, false, true>()
-                                          : vec  ? blocks_per_sm<F, true, NRMF_NT, false>()
-                                                 : blocks_per_sm<F, false, 1, false>());
+                                          : vec     ? blocks_per_sm<F, true, NRMF_NT, false>()
+                                          : eshort  ? blocks_per_sm<F, false, 1, false, false, false, true>()
+                                                    : blocks_per_sm<F, false, 1, false>());
   if (g_grid_override > 0) grid = g_grid_override;
   // warp groups of up to 8 tiles while there is enough work for every warp
   // Small calls: the split kernel (one CTA per group of G tiles, one warp per
@@ -1670,6 +1682,9 @@ static int launch_tree(const F* x, int64_t n_items, int64_t tpc, int64_t ld, int
   } else if (vec) {
     blocks_per_sm<F, true, 1, false>();
     nrmf_tree_kernel<F, true, 1, false><<<(unsigned)grid, kThreads, kernel_smem<F, true>(), s>>>(job);
+  } else if (eshort) {
+    nrmf_tree_kernel<F, false, 1, false, false, false, true>
+        <<<(unsigned)grid, kThreads, kernel_smem<F, false>(), s>>>(job);
   } else {
     nrmf_tree_kernel<F, false, 1, false><<<(unsigned)grid, kThreads, kernel_smem<F, false>(), s>>>(job);
   }

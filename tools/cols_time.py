@@ -29,7 +29,9 @@ for (r, c, ld, dt) in [(4096, 65536, 4096, torch.float64), (4096, 65536, 4160, t
                        (1000, 262144, 1000, torch.float64), (500, 524288, 500, torch.float64), (700, 393216, 700, torch.float64),
                        (1500, 174762, 1500, torch.float32),
                        (1024, 262144, 1024, torch.float64), (2000, 131072, 2000, torch.float32),
-                       (300, 262144, 301, torch.float32), (100, 1 << 20, 100, torch.float64)]:
+                       (300, 262144, 301, torch.float32), (100, 1 << 20, 100, torch.float64),
+                       (100, 1 << 20, 101, torch.float64), (500, 524288, 501, torch.float64),
+                       (4096, 32768, 4097, torch.float64), (4096, 32768, 4097, torch.float32)]:
     B = torch.randn(c, ld, dtype=dt, device="cuda")
     A = B.t()[:r]
     ms = t(A)
