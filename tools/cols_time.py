@@ -25,7 +25,7 @@ def t(A, reps=20):
 for (r, c, ld, dt) in [(4096, 65536, 4096, torch.float64), (4096, 65536, 4160, torch.float64),
                        (8192, 32768, 8192, torch.float64), (8192, 32768, 8256, torch.float64),
                        (4096, 65536, 4160, torch.float32),
-                       (4096, 65536, 4096, torch.float32), (4000, 65536, 4096, torch.float64),
+                       (4096, 65536, 4096, torch.float32), (4000, 65536, 4096, torch.float64), (4000, 65536, 4000, torch.float64), (3000, 65536, 3000, torch.float32),
                        (1000, 262144, 1000, torch.float64), (500, 524288, 500, torch.float64), (700, 393216, 700, torch.float64),
                        (1500, 174762, 1500, torch.float32),
                        (1024, 262144, 1024, torch.float64), (2000, 131072, 2000, torch.float32),
