@@ -45,6 +45,9 @@ constexpr int kMaxFanLg = 8;  // combine steps of 6 levels; the split kernel's l
 #ifndef NRMF_SHORT_PAIRS
 #define NRMF_SHORT_PAIRS 1    // columns of rows <= 2 batches: two per warp at a time
 #endif
+#ifndef NRMF_LL_TWO
+#define NRMF_LL_TWO 1  // split kernel: the fan-in-256 last step polled by two warps
+#endif
 #ifndef NRMF_SHORT_PAIRS_ELEM
 #define NRMF_SHORT_PAIRS_ELEM 1  // ... also in the element-load kernel (unaligned column blocks)
 #endif
@@ -436,13 +439,118 @@ __device__ __noinline__ F ll_gather_combine(char* ll, int64_t nin, int f, int cr
   }
   return v;
 }
+// Fan-in 256 split over two polling warps (CTA 0's warps 1 and 2): warp
+// `half` polls slots [128 half, 128 half + 128), 4 per lane (a poll round of
+// 4 loads per lane returns sooner than one of 8 under load), clears them and
+// evaluates its 128-input subtree (2 in-lane + 5 shuffle levels, checked fast
+// nodes).  Warp 2 leaves its raw inputs, value and flag in xch[0..129] and
+// meets warp 1 at named barrier 1; warp 1 evaluates the top node, or -- any
+// flagged node or NaN -- the whole 256-input subtree with exact nodes from its
+// registers and xch.  The same tree as ll_gather_combine<F, 8>.  Returns the
+// root in warp 1 (meaningless in warp 2).
 template <typename F>
-__device__ void ll_combine(const TreeJob<F>& job, uint64_t call) {
+__device__ __noinline__ F ll_gather_half(char* ll, int64_t nin, int cr, uint64_t tag, int half, F* xch) {
+  constexpr int KP = 4;
+  const uint32_t t1 = (uint32_t)tag, t2 = (uint32_t)(tag >> 32);
+  const int lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)half * 128 + (int64_t)lane * KP;
+  F a[KP];
+  bool ready[KP];
+#pragma unroll
+  for (int j = 0; j < KP; ++j) {
+    a[j] = F(0);
+    ready[j] = !(base + j < nin);
+  }
+  for (long long spins = 0;; ++spins) {
+    uint32_t lo[KP], e0[KP], hi[KP], e1[KP];
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      const int64_t i = base + j < nin ? base + j : (nin > 0 ? nin - 1 : 0);
+      ld_ll_gpu(ll + 16 * (i + 1), lo[j], e0[j], hi[j], e1[j]);
+    }
+    bool all = true;
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      if (ready[j]) continue;
+      if (e0[j] == t1 && e1[j] == t2) {
+        a[j] = from_words<F>(lo[j], hi[j]);
+        ready[j] = true;
+      } else {
+        all = false;
+      }
+    }
+    if (__all_sync(0xffffffffu, all)) break;
+    if (spins > (1ll << 26)) {  // never: every producer of the step writes its slot
+#pragma unroll
+      for (int j = 0; j < KP; ++j)
+        if (!ready[j]) a[j] = sizeof(F) == 8 ? F(__longlong_as_double(0x7ff8000000000000ll)) : F(__int_as_float(0x7fc00000));
+      break;
+    }
+    if (spins > 32) __nanosleep(32);
+  }
+  bool bad = cr != 0;
+  F v = F(0);
+  if (!bad) {
+    F b[KP];
+#pragma unroll
+    for (int j = 0; j < KP; ++j) b[j] = a[j];
+    in_lane_levels<F, KP>(b, bad);
+    v = b[0];
+    for (int l = 0; l < 5; ++l) v = v1h_fast<true>(v, __shfl_xor_sync(0xffffffffu, v, 1 << l), bad);
+    bad = __any_sync(0xffffffffu, bad || v != v);
+  }
+#pragma unroll
+  for (int j = 0; j < KP; ++j)
+    if (base + j < nin) st_ll2_gpu(ll + 16 * (base + j + 1), 0u, 0u, 0u, 0u);
+  if (half == 1) {
+#pragma unroll
+    for (int j = 0; j < KP; ++j) xch[lane * KP + j] = a[j];
+    if (lane == 0) {
+      xch[128] = v;
+      xch[129] = bad ? F(1) : F(0);
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    return v;
+  }
+  asm volatile("bar.sync 1, 64;" ::: "memory");
+  const F v1 = xch[128];
+  bool bad2 = bad || xch[129] != F(0);
+  F root = F(0);
+  if (!bad2) {
+    root = v1h_fast<true>(v, v1, bad2);
+    bad2 = bad2 || root != root;
+  }
+  if (bad2) {  // the whole subtree with exact nodes (v1_hypot or cr_hypot)
+    F e[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      F c[KP];
+#pragma unroll
+      for (int j = 0; j < KP; ++j) c[j] = hh == 0 ? a[j] : xch[lane * KP + j];
+#pragma unroll
+      for (int st = 1; st < KP; st <<= 1)
+#pragma unroll
+        for (int j = 0; j < KP; j += 2 * st) c[j] = top_node(c[j], c[j + st], cr);
+      F w = c[0];
+      for (int l = 0; l < 5; ++l) w = top_node(w, __shfl_xor_sync(0xffffffffu, w, 1 << l), cr);
+      e[hh] = w;
+    }
+    root = top_node(e[0], e[1], cr);
+  }
+  return root;
+}
+
+template <typename F>
+__device__ void ll_combine(const TreeJob<F>& job, uint64_t call, F* xch = nullptr) {
   const int K = job.nsteps - 1;
   const int f = job.lg_fan[K];
   const uint64_t tag = ll_tag(job.ll, call);
   NRMF_TRACE(6, 0, 0);
   F v;
+  if (NRMF_LL_TWO && f == 8 && xch != nullptr) {
+    v = ll_gather_half<F>(job.ll, job.nin[K], job.top_cr, tag, (threadIdx.x >> 5) == 2 ? 1 : 0, xch);
+    if ((threadIdx.x >> 5) == 2) return;  // warp 2: its half is in xch
+  } else
   switch (f) {
     case 8: v = ll_gather_combine<F, 8>(job.ll, job.nin[K], f, job.top_cr, tag); break;
     case 7: v = ll_gather_combine<F, 4>(job.ll, job.nin[K], f, job.top_cr, tag); break;
@@ -1225,10 +1333,14 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   const int k = w / NIT, it = w % NIT;
   NRMF_TRACE(0, 0, 0);
   const bool ll_comb = job.ll != nullptr && blockIdx.x == 0 && w == 1;
+  // fan-in 256: warp 2 polls the upper half of the slots (ll_gather_half)
+  const bool ll_two = NRMF_LL_TWO && job.ll != nullptr && blockIdx.x == 0 && job.nsteps >= 1 &&
+                      job.lg_fan[job.nsteps - 1] == 8;
+  __shared__ F ll_xch[130];
   // this call's number (the combiner; the producers' slot tag is hashed from
   // it after the batch phase): the header load -- a DRAM round trip with a
   // cold L2 -- is issued behind the batch loads, not ahead of them
-  const bool need_hdr = job.ll != nullptr && (w == 0 || ll_comb);
+  const bool need_hdr = job.ll != nullptr && (w == 0 || ll_comb || (ll_two && w == 2));
   uint64_t ll_c = 0;
   // are all G tiles of the group full tiles with data?
   bool full = (grp + 1) * G <= job.n_items;
@@ -1266,7 +1378,11 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 2) nrmf_split_kernel(const T
   NRMF_TRACE(15, 0, 0);
   if (ll_comb) {
     if (job.peers != nullptr) prefetch_exchange(job.peers, job.p_rank);  // it polls long before the root
-    ll_combine(job, ll_c);
+    ll_combine(job, ll_c, ll_two ? ll_xch : (F*)nullptr);
+    return;
+  }
+  if (ll_two && w == 2) {
+    ll_combine(job, ll_c, ll_xch);
     return;
   }
   if (w != 0) return;

@@ -68,7 +68,8 @@ def main():
             spins = a[:, 7][a[:, 7] > 0]
             acc.setdefault("spins", []).append(spins)
         L.nrmf_debug_set_trace(None, 0)
-        print("  poll rounds per call:", [int(v[0]) for v in acc["spins"]])
+        print("  poll rounds per call:", [int(v[0]) if len(v) else None for v in acc["spins"]],
+              "(None: the two-warp last step records no round count)")
         print(f"== {dt} n=2^{lg}: event-timed median {np.median(tot):.1f} us over {reps} calls "
               f"(last {reps - 1} averaged below)")
         for k, name in NAMES.items():
